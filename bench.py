@@ -1,0 +1,389 @@
+"""Benchmark of the Q-Palette fused dequant-GEMV hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N    (row-sharded layers + NCCL all-gather)
+
+Workload (BASELINE.json configs[1], "C2"): the Llama-3.1-8B layer shapes (d_out, d_in) =
+(4096, 4096), (14336, 4096), (4096, 14336), each at TCQ 2.5 / half-TCQ 3.25 / TCQ 4.0 bits
+(L = 16), batch 1, synthetic uniform-random codes (= Gaussianized weights, DESIGN.md input
+recipe), x ~ N(0,1) fp16. One step = for each of the 9 layers: the activation rotation
+kernel + the fused dequant-GEMV kernel (qp_linear_fwd), captured once in a CUDA graph.
+Metric: achieved HBM GB/s on the algorithmic (compressed) bytes of the step, plus us/layer.
+Two replicas of every layer alternate between steps (326 MB > 126 MB L2: inputs larger
+than L2). With N > 1 every layer is row-sharded over the ranks and each forward ends with
+an NCCL all-gather of y (strong scaling; total work fixed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("fused dequant-GEMV µs/layer and achieved HBM GB/s vs ~8 TB/s, batch 1–8, 1/2/4/8 B200")
+SHAPES = [(4096, 4096), (14336, 4096), (4096, 14336)]
+WIDTHS = [("tcq", 10), ("half_tcq", 13), ("tcq", 16)]
+BATCH = 1
+SEED = 7
+REPLICAS = 2
+
+
+def tlut_file(scheme: str, bits_x4: int) -> str:
+    b = (bits_x4 + 1) / 4 if scheme == "half_tcq" else bits_x4 / 4     # half-TCQ: upper width's tlut
+    tb = 9 if b <= 4 else (10 if b <= 4.5 else 11)
+    return os.path.join(ROOT, "codebooks", f"tcq_tlut_tb{tb}.f16"), tb
+
+
+def code_bytes(d_out: int, d_in: int, bits_x4: int) -> int:
+    return d_out * d_in * bits_x4 // 32
+
+
+def layer_bytes(d_out, d_in, bits_x4, tb, batch):
+    """Algorithmic bytes: codes + fp32 scales + compressed LUT + x' in + y out."""
+    gemv = code_bytes(d_out, d_in, bits_x4) + 4 * d_out + (4 << tb) + 2 * batch * d_in + 4 * batch * d_out
+    rht = 4 * batch * d_in            # read x fp16, write x' fp16
+    return gemv, rht
+
+
+def workload(world=1):
+    out = []
+    for d_out, d_in in SHAPES:
+        for scheme, x4 in WIDTHS:
+            _, tb = tlut_file(scheme, x4)
+            out.append(dict(d_out=d_out, d_in=d_in, scheme=scheme, bits_x4=x4, tb=tb, m=d_out // world))
+    return out
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for n, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def oracle_sample(layers, budget_rows=512):
+    """CPU baseline: the float64 oracle (decode + RHT + matvec) on a bounded sample."""
+    import oracle.decode as odec
+    import oracle.rht as orht
+    from oracle import codebooks as ocb
+    from qp_synth import activations_fp16, channel_scales, random_code_bytes
+    total_bytes, t0 = 0, time.perf_counter()
+    for li, L in enumerate(layers):
+        d_out, d_in, scheme, x4, tb = L["d_out"], L["d_in"], L["scheme"], L["bits_x4"], L["tb"]
+        tl = np.fromfile(tlut_file(scheme, x4)[0], dtype="<f2").astype(np.float64).reshape(-1, 2)
+        book = {"lut": ocb.quantlut_sym(tl, 16, tb), "L": 16}
+        rows = min(budget_rows, d_out)
+        nb = code_bytes(rows, d_in, x4)
+        codes = random_code_bytes(nb, li)
+        x = activations_fp16(BATCH, d_in).astype(np.float64)
+        s = channel_scales(d_out, d_in)[:rows]
+        W = odec.decode_layer(codes, rows, d_in, scheme, x4, book)
+        y = (orht.rht_apply(x, SEED) @ W.T) * s[None, :]
+        assert np.isfinite(y).all()
+        g, r = layer_bytes(rows, d_in, x4, tb, BATCH)
+        total_bytes += g + r
+    dt = time.perf_counter() - t0
+    return total_bytes, dt
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        th = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        th = os.cpu_count() or 1
+    return th
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    layers = workload(1)
+    times, nbytes = [], 0
+    for i in range(args.warmup + args.steps):
+        nb, dt = oracle_sample(layers, budget_rows=64)
+        if i >= args.warmup:
+            times.append(dt)
+            nbytes = nb
+    t = statistics.mean(times)
+    v = nbytes / t / 1e9
+    cores = cpu_cores()
+    line = {"metric": METRIC, "value": round(v, 6), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "C2 Llama-3.1-8B shapes x TCQ 2.5/3.25/4.0, batch 1 (64-row sample per layer)",
+                       "batch": BATCH},
+            "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": cores, "kind": "oracle",
+                             "sample": "first 64 rows of each of the 9 layers: decode + RHT + matvec, float64"},
+            "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2509_20214_b200 import _lib as QL
+    from qp_synth import activations_fp16, channel_scales, random_code_bytes
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    batch = args.batch
+    layers = workload(world)
+    cbs = {}
+    for L in layers:
+        key = (L["scheme"], L["bits_x4"])
+        if key not in cbs:
+            cbs[key] = QL.Codebook(L["scheme"], L["bits_x4"], np.fromfile(tlut_file(*key)[0], dtype="<f2"), L=16)
+    rots = {d_in: QL.Rht(SEED, d_in) for _, d_in in SHAPES}
+    comm = None
+    if world > 1:
+        uid = [QL.NcclComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = QL.NcclComm(uid[0], world, rank)
+
+    # layers (replicas x 9), each rank holding its row shard
+    insts = []
+    for rep in range(REPLICAS):
+        for li, L in enumerate(layers):
+            d_out, d_in = L["d_out"], L["d_in"]
+            codes = random_code_bytes(code_bytes(d_out, d_in, L["bits_x4"]), 100 * rep + li)
+            s = channel_scales(d_out, d_in)
+            full = QL.Layer.from_codes(codes, s, d_out, d_in, L["scheme"], L["bits_x4"], cbs[(L["scheme"], L["bits_x4"])],
+                                       rots[d_in])
+            lay = full.shard(rank, world) if world > 1 else full
+            if world > 1:
+                del full
+            x = torch.from_numpy(activations_fp16(batch, d_in)).to(dev)
+            y = torch.empty(batch, d_out, dtype=torch.float32, device=dev)
+            insts.append(dict(layer=lay, x=x, y=y, meta=L))
+    torch.cuda.synchronize()
+
+    def fwd(inst, stream=None, flags=0):
+        if world > 1:
+            inst["layer"].forward_sharded(inst["x"], batch, inst["y"], comm, flags=flags, stream=stream)
+        else:
+            inst["layer"].forward(inst["x"], batch, inst["y"], flags=flags, stream=stream)
+
+    # ---- capture one graph per replica ------------------------------------------------
+    stream = torch.cuda.Stream(device=dev)
+    n_layers = len(layers)
+    graphs = []
+    with torch.cuda.stream(stream):
+        for rep in range(REPLICAS):
+            for inst in insts[rep * n_layers:(rep + 1) * n_layers]:
+                fwd(inst, stream)          # eager warm-up (sets kernel attributes)
+        stream.synchronize()
+        for rep in range(REPLICAS):
+            g = torch.cuda.CUDAGraph()
+            c0 = QL.launch_count()
+            with torch.cuda.graph(g, stream=stream):
+                for inst in insts[rep * n_layers:(rep + 1) * n_layers]:
+                    fwd(inst, stream)
+            launches_per_step = QL.launch_count() - c0
+            graphs.append(g)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        graphs[i % REPLICAS].replay()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        ev0.record(stream)
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                graphs[i % REPLICAS].replay()
+        ev1.record(stream)
+        ev1.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # algorithmic bytes of one step (whole job: all ranks' shards = the full layers)
+    gemv_bytes = rht_bytes = 0
+    for L in layers:
+        g_, r_ = layer_bytes(L["d_out"], L["d_in"], L["bits_x4"], L["tb"], batch)
+        gemv_bytes += g_
+        rht_bytes += r_ * world                # every rank rotates its own copy of x
+    step_bytes = gemv_bytes + rht_bytes
+    value = step_bytes / (ms * 1e-3) / 1e9
+
+    # ---- per-kernel timing of the fused GEMV (pre-rotated x, no PDL, events per launch) -----
+    xr = {}
+    for inst in insts:
+        d_in = inst["meta"]["d_in"]
+        if d_in not in xr:
+            xr[d_in] = torch.empty(batch, d_in, dtype=torch.float16, device=dev)
+            rots[d_in].apply(inst["x"], batch, xr[d_in])
+    torch.cuda.synchronize()
+    gemv_ms = []
+    gemv_alg = 0
+    with torch.cuda.stream(stream):
+        evs = []
+        reps_k = max(3, min(args.steps, 10))
+        for it in range(reps_k + 1):
+            for inst in insts:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                inst["layer"].forward(xr[inst["meta"]["d_in"]], batch, inst["y"],
+                                      flags=QL.QP_X_PREROTATED | QL.QP_NO_PDL, stream=stream)
+                b.record(stream)
+                if it > 0:
+                    evs.append((a, b, inst))
+        stream.synchronize()
+    for a, b, inst in evs:
+        gemv_ms.append(a.elapsed_time(b))
+        L = inst["meta"]
+        gemv_alg += layer_bytes(L["m"], L["d_in"], L["bits_x4"], L["tb"], batch)[0]
+    gemv_avg_ms = statistics.mean(gemv_ms)
+    gemv_achieved = gemv_alg / (sum(gemv_ms) * 1e-3) / 1e9
+    peak, peak_kind = measured_peaks()
+    per_layer_us = {}
+    for (a, b, inst) in evs:
+        L = inst["meta"]
+        k = f'{L["d_out"]}x{L["d_in"]}@{L["bits_x4"] / 4:g}b'
+        per_layer_us.setdefault(k, []).append(a.elapsed_time(b) * 1e3)
+    per_layer_us = {k: round(statistics.median(v), 2) for k, v in per_layer_us.items()}
+
+    # ---- end to end through the public API with host buffers (N=1 only) ------------------
+    e2e = None
+    if world == 1:
+        hx = [torch.from_numpy(activations_fp16(batch, L["d_in"])).pin_memory() for L in layers]
+        hy = [torch.empty(batch, L["d_out"], dtype=torch.float32).pin_memory() for L in layers]
+        h2d = sum(t.numel() * 2 for t in hx)
+        d2h = sum(t.numel() * 4 for t in hy)
+        with torch.cuda.stream(stream):
+            def e2e_step(rep):
+                for j, inst in enumerate(insts[rep * n_layers:(rep + 1) * n_layers]):
+                    inst["x"].copy_(hx[j], non_blocking=True)
+                    fwd(inst, stream)
+                    hy[j].copy_(inst["y"], non_blocking=True)
+            for i in range(args.warmup):
+                e2e_step(i % REPLICAS)
+            stream.synchronize()
+            t0 = time.perf_counter()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(args.steps):
+                e2e_step(i % REPLICAS)
+            e1.record(stream)
+            e1.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.steps
+        e2e = {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nb, dt = oracle_sample(layers, budget_rows=512)
+        cpu = {"value": round(nb / dt / 1e9, 6), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": "first 512 rows of each of the 9 C2 layers: float64 decode + RHT + matvec (batch 1)",
+               "seconds": round(dt, 2)}
+
+    if rank == 0:
+        ck = clk.summary()
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "config": {"workload": "C2: Llama-3.1-8B (4096x4096, 14336x4096, 4096x14336) x TCQ-2.5 / half-TCQ-3.25 / "
+                                   "TCQ-4.0 (L=16), RHT + fused dequant-GEMV per layer",
+                       "batch": batch, "layers_per_step": n_layers, "us_per_layer": round(ms * 1e3 / n_layers, 3),
+                       "parallelism": f"row-shard x{world} + NCCL all-gather" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (2 replicas, 326 MB per 2 steps, L2 126 MB)",
+                       "graph": "CUDA graph per step, PDL between the rotation and GEMV kernels",
+                       "gemv_us_per_layer": per_layer_us},
+            "roofline": {"bound": "hbm", "achieved": round(gemv_achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gemv_achieved / peak, 4), "traffic": None,
+                         "kernel": "qp_gemv_kernel (fused dequant-GEMV), all 9 layers, events per launch",
+                         "peak_kind": peak_kind, "avg_launch_us": round(gemv_avg_ms * 1e3, 3)},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches_per_step * args.steps),
+            "clocks": ck,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,170 @@
+/*
+ * qpalette.h -- C ABI of the B200 (sm_100a) Q-Palette hot path.
+ *
+ * What the library computes (Q-Palette, arXiv 2509.20214; "P:n" = line n of the
+ * paper source /root/reference/PAPER.md, "S:n" = line n of SPEC.md):
+ *
+ *     y[beta] = diag(s) * W_hat * (R x[beta]),   beta = 0 .. batch-1,  batch in 1..8
+ *
+ *   R      randomized Hadamard rotation of the input dimension only:
+ *          R = (1/sqrt(b)) * blockdiag(H_b, ..., H_b) * D, H_b Sylvester, D = diag(+-1)
+ *          drawn from splitmix64(seed, i); b = largest power-of-two divisor of d_in.
+ *   W_hat  weights decoded on the fly from fractional-bit codes:
+ *          TCQ / half-TCQ (bitshift trellis, hybrid `quantlut_sym` codebook, tail-biting),
+ *          2-D VQ, NUQ and uniform scalar quantization.
+ *   s      per-output-channel scales.
+ *
+ * Code layout: LAYOUT.md (tiles of 32 rows x 256 columns, row-tile-major, one trellis /
+ * code run of 256 weights per lane, MSB-first 32-bit word streams).
+ *
+ * Conventions (apply to every entry point):
+ *   - Ownership: the caller owns x, y, W and every host buffer; the library owns the
+ *     device memory of codebooks, rotations, layers and groups (allocated through the
+ *     hook of qp_set_allocator if set, else cudaMalloc) and frees it in qp_*_free.
+ *     A layer references (does not own) its codebook and rotation: free layers first.
+ *   - Asynchrony: argument/shape validation is synchronous and returns a status; all
+ *     device work is enqueued on `stream` (a cudaStream_t, passed as void*) with no
+ *     implicit synchronisation. Asynchronous CUDA faults surface as QP_ERR_CUDA on a
+ *     later call. A layer or group object may be used by one stream at a time (it owns
+ *     a small scratch buffer); distinct objects may be used concurrently.
+ *   - Errors: every call returns a qp_status; qp_last_error() returns a thread-local
+ *     message with a one-line remedy. No call aborts the process.
+ *   - There is no CPU fallback: device entry points fail with QP_ERR_CUDA when no
+ *     sm_100 device is present.
+ *   - Widths (bits_x4 = 4 * bits per weight; Table 1, plus uniform SQ):
+ *       QP_TCQ       1.5 .. 5.0  step 0.5   (bits_x4 6,8,..,20; shift s = 2b)
+ *       QP_HALF_TCQ  1.75 .. 4.75 step 0.5  (bits_x4 7,9,..,19; d_in halves at b, b+0.5)
+ *       QP_VQ        1.5 .. 6.0  step 0.5   (bits_x4 6,8,..,24; 2b-bit index per pair)
+ *       QP_NUQ       2 .. 8                 (bits_x4 8,12,..,32)
+ *       QP_UNIF      2 .. 8                 (bits_x4 8,12,..,32)
+ *     others -> QP_ERR_UNSUPPORTED_WIDTH.
+ *   - Partition (else QP_ERR_PARTITION_MISMATCH): d_out % 32 == 0, d_in % 256 == 0,
+ *     half-TCQ also (d_in / 2) % 256 == 0; batch in 1..8 ("batch sizes up to 8").
+ */
+#ifndef QPALETTE_H
+#define QPALETTE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QP_OK = 0,
+  QP_ERR_INVALID_ARG = 1,        /* null pointer, negative size, bad enum            */
+  QP_ERR_UNSUPPORTED_WIDTH = 2,  /* scheme/bits_x4 not in Table 1             */
+  QP_ERR_PARTITION_MISMATCH = 3, /* shapes not multiples of the tile         */
+  QP_ERR_DIM = 4,                /* incompatible dimensions                   */
+  QP_ERR_CONFIG_MISMATCH = 5,    /* codebook / rotation do not match the layer*/
+  QP_ERR_LENGTH = 6,             /* byte count does not match the layout     */
+  QP_ERR_ALLOC = 7,              /* device allocation failed                         */
+  QP_ERR_CUDA = 8,               /* CUDA runtime error (incl. no sm_100 device)      */
+  QP_ERR_NCCL = 9,               /* NCCL error                                       */
+  QP_ERR_UNSUPPORTED = 10        /* valid request this build does not implement      */
+} qp_status;
+
+typedef enum { QP_NUQ = 0, QP_UNIF = 1, QP_VQ = 2, QP_TCQ = 3, QP_HALF_TCQ = 4 } qp_scheme;
+typedef enum { QP_F16 = 0, QP_BF16 = 1, QP_F32 = 2 } qp_dtype;
+
+/* flags of the forward calls */
+#define QP_X_PREROTATED 1u   /* x is already R x in fp16 (skip the rotation kernel) */
+#define QP_NO_PDL 2u         /* launch without programmatic dependent launch        */
+#define QP_DETERMINISTIC 4u  /* fp32 y: in-order cross-CTA reduction (bitwise reproducible) instead of
+                                zero-then-atomic-add (fp16 y is always in-order)        */
+
+typedef struct qp_codebook qp_codebook;
+typedef struct qp_rht qp_rht;
+typedef struct qp_layer qp_layer;
+typedef struct qp_group qp_group;
+
+/* Route the library's device allocations (e.g. to PyTorch's caching allocator).
+ * alloc(size, ctx) returns a device pointer or NULL; free_(ptr, ctx). Pass NULLs to
+ * restore cudaMalloc/cudaFree. Must be called before objects are created. */
+qp_status qp_set_allocator(void* (*alloc)(size_t, void*), void (*free_)(void*, void*), void* ctx);
+
+/* Load a frozen fp16 codebook (host memory, little-endian IEEE half, row-major).
+ *   QP_TCQ / QP_HALF_TCQ: tlut [2^tb][2] of TCQ at the (upper) width, tb = 9 for b <= 4,
+ *        10 for 4.5, 11 for 5.0; the hybrid LUT is quantlut_sym(tlut, L, tb)
+ *        (P:1025-1033), L in {12, 16} (L = 16 is the paper's; 12 is config C1).
+ *   QP_VQ: LUT [2^(2b)][2].   QP_NUQ / QP_UNIF: LUT [2^b].
+ * n_bytes must equal the table size (else QP_ERR_LENGTH). L is ignored for non-TCQ. */
+qp_status qp_codebook_load(qp_scheme scheme, int bits_x4, int L, const void* host_fp16, size_t n_bytes,
+                           qp_codebook** out);
+void qp_codebook_free(qp_codebook* cb);
+
+/* Rotation R for inputs of width d_in. block = 0 selects the largest
+ * power-of-two divisor of d_in; otherwise block must be a power of two dividing d_in. */
+qp_status qp_rht_create(uint64_t seed, int d_in, int block, qp_rht** out);
+void qp_rht_free(qp_rht* r);
+
+/* x_rot[batch][d_in] (fp16, device) = R x (x device, [batch][d_in] of dtype xt).
+ * Arithmetic in fp32, one rounding to fp16 at the end. */
+qp_status qp_rht_apply(const qp_rht* r, const void* x, qp_dtype xt, int batch, void* x_rot, void* stream);
+
+/* Layer from packed codes (host, LAYOUT.md order, exactly d_out*d_in*bits/8 bytes) and
+ * fp32 per-output-channel scales (host, d_out). Copies both to the device. */
+qp_status qp_layer_from_codes(const void* codes_host, size_t n_bytes, const float* scales_host, int d_out, int d_in,
+                              qp_scheme scheme, int bits_x4, const qp_codebook* cb, const qp_rht* r, qp_layer** out);
+
+/* Data-free quantization of an nn.Linear weight W[d_out][d_in] (host fp32, row-major)
+ * (P:348): W' = W R^T, s_j = RMS(W'_j), W~ = W'/s, then RTN (NUQ, UNIF, VQ) or the
+ * rotate-half tail-biting Viterbi (TCQ, half-TCQ; reading R4), on n_threads
+ * host threads (0 = all). Host-side and slow at L = 16; the GPU encoder
+ * is future work. */
+qp_status qp_quantize_offline(const float* W_host, int d_out, int d_in, qp_scheme scheme, int bits_x4,
+                              const qp_codebook* cb, const qp_rht* r, int n_threads, qp_layer** out);
+
+/* Copy a layer's codes / scales back to the host (n_bytes must equal the stored size). */
+qp_status qp_layer_get_codes(const qp_layer* l, void* codes_host, size_t n_bytes);
+qp_status qp_layer_get_scales(const qp_layer* l, float* scales_host);
+
+/* y[batch][d_out] (device, dtype yt in {F16, F32}) = diag(s) W_hat R x (the fused
+ * dequantize-and-multiply). x: device [batch][d_in] of dtype xt, or R x in
+ * fp16 with QP_X_PREROTATED. Two kernels: rotation + fused GEMV (PDL-chained). */
+qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch, void* y, qp_dtype yt,
+                        unsigned flags, void* stream);
+
+/* Fused group: members share d_in, rotation, scheme, width and codebook
+ * (e.g. q/k/v or up/gate). One GEMV launch over the concatenated rows; ys[i] receives
+ * member i's rows ([batch][d_out_i]). Members are copied; they may be freed afterwards. */
+qp_status qp_fuse(const qp_layer* const* members, int n, qp_group** out);
+void qp_group_free(qp_group* g);
+qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int batch, void* const* ys, qp_dtype yt,
+                          unsigned flags, void* stream);
+
+/* W_hat[d_out][d_in] (device fp16) without scales: the dequantization-only kernel
+ * (P:1154-1163). Bit-exact against the oracle's decode (frozen fp16 codebooks). */
+qp_status qp_dequantize(const qp_layer* l, void* W_hat_fp16, void* stream);
+
+/* Contiguous row block [rank*d_out/world, (rank+1)*d_out/world) of a layer as a new
+ * layer (device copy). (d_out/world) % 32 must be 0. */
+qp_status qp_layer_shard(const qp_layer* l, int rank, int world, qp_layer** out);
+
+/* NCCL plumbing for the row-sharded path (NCCL over NVLink / NVSwitch).
+ * qp_nccl_unique_id writes 128 bytes; broadcast them (e.g. with torch.distributed)
+ * and call qp_nccl_comm_create on every rank. comm is an ncclComm_t. */
+qp_status qp_nccl_unique_id(void* id128);
+qp_status qp_nccl_comm_create(const void* id128, int world, int rank, void** comm);
+qp_status qp_nccl_comm_destroy(void* comm);
+
+/* Row-sharded forward: this rank computes its shard's rows, then an all-gather over
+ * `comm` assembles y_full[batch][d_out_full] (device, dtype yt) on every rank. */
+qp_status qp_linear_fwd_sharded(const qp_layer* shard, const void* x, qp_dtype xt, int batch, void* y_full,
+                                qp_dtype yt, void* comm, unsigned flags, void* stream);
+
+/* Introspection. bits_per_weight counts code bits only (reading R19). */
+qp_status qp_layer_info(const qp_layer* l, size_t* code_bytes, double* bits_per_weight, int* d_out, int* d_in);
+
+/* Number of kernels the library has enqueued since load (for launch accounting). */
+uint64_t qp_launch_count(void);
+
+void qp_layer_free(qp_layer* l);
+const char* qp_last_error(void);
+const char* qp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QPALETTE_H */

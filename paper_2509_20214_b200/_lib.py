@@ -1,0 +1,252 @@
+"""ctypes binding of libqpalette.so (include/qpalette.h): argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only converts
+Python objects (torch tensors for device memory, numpy arrays for host memory) into the
+pointers and sizes of the C ABI. If the shared library is missing it raises -- there is
+no Python or CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libqpalette.so")
+
+QP_OK = 0
+STATUS = {0: "QP_OK", 1: "QP_ERR_INVALID_ARG", 2: "QP_ERR_UNSUPPORTED_WIDTH", 3: "QP_ERR_PARTITION_MISMATCH",
+          4: "QP_ERR_DIM", 5: "QP_ERR_CONFIG_MISMATCH", 6: "QP_ERR_LENGTH", 7: "QP_ERR_ALLOC", 8: "QP_ERR_CUDA",
+          9: "QP_ERR_NCCL", 10: "QP_ERR_UNSUPPORTED"}
+SCHEMES = {"nuq": 0, "unif": 1, "vq": 2, "tcq": 3, "half_tcq": 4}
+DTYPES = {"f16": 0, "bf16": 1, "f32": 2}
+QP_X_PREROTATED = 1
+QP_NO_PDL = 2
+QP_DETERMINISTIC = 4
+
+# every symbol include/qpalette.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "qp_set_allocator", "qp_codebook_load", "qp_codebook_free", "qp_rht_create", "qp_rht_free", "qp_rht_apply",
+    "qp_layer_from_codes", "qp_quantize_offline", "qp_layer_get_codes", "qp_layer_get_scales", "qp_linear_fwd",
+    "qp_fuse", "qp_group_free", "qp_fused_linear", "qp_dequantize", "qp_layer_shard", "qp_nccl_unique_id",
+    "qp_nccl_comm_create", "qp_nccl_comm_destroy", "qp_linear_fwd_sharded", "qp_layer_info", "qp_launch_count",
+    "qp_layer_free", "qp_last_error", "qp_version",
+]
+
+
+class QPError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2509_20214_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i, sz, u64 = C.c_void_p, C.c_int, C.c_size_t, C.c_uint64
+        sig = {
+            "qp_codebook_load": [i, i, i, vp, sz, C.POINTER(vp)],
+            "qp_codebook_free": [vp],
+            "qp_rht_create": [u64, i, i, C.POINTER(vp)],
+            "qp_rht_free": [vp],
+            "qp_rht_apply": [vp, vp, i, i, vp, vp],
+            "qp_layer_from_codes": [vp, sz, vp, i, i, i, i, vp, vp, C.POINTER(vp)],
+            "qp_quantize_offline": [vp, i, i, i, i, vp, vp, i, C.POINTER(vp)],
+            "qp_layer_get_codes": [vp, vp, sz],
+            "qp_layer_get_scales": [vp, vp],
+            "qp_linear_fwd": [vp, vp, i, i, vp, i, C.c_uint, vp],
+            "qp_fuse": [C.POINTER(vp), i, C.POINTER(vp)],
+            "qp_group_free": [vp],
+            "qp_fused_linear": [vp, vp, i, i, C.POINTER(vp), i, C.c_uint, vp],
+            "qp_dequantize": [vp, vp, vp],
+            "qp_layer_shard": [vp, i, i, C.POINTER(vp)],
+            "qp_nccl_unique_id": [vp],
+            "qp_nccl_comm_create": [vp, i, i, C.POINTER(vp)],
+            "qp_nccl_comm_destroy": [vp],
+            "qp_linear_fwd_sharded": [vp, vp, i, i, vp, i, vp, C.c_uint, vp],
+            "qp_layer_info": [vp, C.POINTER(sz), C.POINTER(C.c_double), C.POINTER(i), C.POINTER(i)],
+            "qp_layer_free": [vp],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = None if name.endswith("_free") and name != "qp_nccl_comm_destroy" else C.c_int
+        L.qp_last_error.restype = C.c_char_p
+        L.qp_version.restype = C.c_char_p
+        L.qp_launch_count.restype = C.c_uint64
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != QP_OK:
+        raise QPError(status, lib().qp_last_error().decode())
+
+
+def launch_count() -> int:
+    return int(lib().qp_launch_count())
+
+
+def _ptr(t) -> int:
+    """Device (torch) or host (numpy) buffer -> address."""
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data
+    assert t.is_contiguous(), "tensors passed to the C ABI must be contiguous"
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dtype_code(t) -> int:
+    import torch
+    return {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2}[t.dtype]
+
+
+class Codebook:
+    """qp_codebook_load: frozen fp16 table (host) -> device decode table."""
+
+    def __init__(self, scheme: str, bits_x4: int, table_fp16: np.ndarray, L: int = 16):
+        t = np.ascontiguousarray(table_fp16, dtype="<f2")
+        h = C.c_void_p()
+        check(lib().qp_codebook_load(SCHEMES[scheme], bits_x4, L, t.ctypes.data, t.nbytes, C.byref(h)))
+        self.h, self.scheme, self.bits_x4, self.L = h, scheme, bits_x4, L
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.qp_codebook_free(self.h)
+            self.h = None
+
+
+class Rht:
+    """qp_rht_create / qp_rht_apply."""
+
+    def __init__(self, seed: int, d_in: int, block: int = 0):
+        h = C.c_void_p()
+        check(lib().qp_rht_create(seed, d_in, block, C.byref(h)))
+        self.h, self.seed, self.d_in = h, seed, d_in
+
+    def apply(self, x, batch: int, out, stream=None) -> None:
+        check(lib().qp_rht_apply(self.h, _ptr(x), _dtype_code(x), batch, _ptr(out), _stream(stream)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.qp_rht_free(self.h)
+            self.h = None
+
+
+class Layer:
+    """A quantized linear layer (qp_layer)."""
+
+    def __init__(self, handle, codebook: Codebook, rht: Rht):
+        self.h = handle
+        self._keep = (codebook, rht)
+        cb, bpw, do, di = C.c_size_t(), C.c_double(), C.c_int(), C.c_int()
+        check(lib().qp_layer_info(self.h, C.byref(cb), C.byref(bpw), C.byref(do), C.byref(di)))
+        self.code_bytes, self.bits_per_weight, self.d_out, self.d_in = cb.value, bpw.value, do.value, di.value
+
+    @classmethod
+    def from_codes(cls, codes: np.ndarray, scales: np.ndarray, d_out: int, d_in: int, scheme: str, bits_x4: int,
+                   codebook: Codebook, rht: Rht) -> "Layer":
+        codes = np.ascontiguousarray(codes, dtype=np.uint8)
+        scales = np.ascontiguousarray(scales, dtype=np.float32)
+        h = C.c_void_p()
+        check(lib().qp_layer_from_codes(codes.ctypes.data, codes.nbytes, scales.ctypes.data, d_out, d_in,
+                                        SCHEMES[scheme], bits_x4, codebook.h, rht.h, C.byref(h)))
+        return cls(h, codebook, rht)
+
+    @classmethod
+    def quantize_offline(cls, W: np.ndarray, scheme: str, bits_x4: int, codebook: Codebook, rht: Rht,
+                         n_threads: int = 0) -> "Layer":
+        W = np.ascontiguousarray(W, dtype=np.float32)
+        h = C.c_void_p()
+        check(lib().qp_quantize_offline(W.ctypes.data, W.shape[0], W.shape[1], SCHEMES[scheme], bits_x4,
+                                        codebook.h, rht.h, n_threads, C.byref(h)))
+        return cls(h, codebook, rht)
+
+    def codes(self) -> np.ndarray:
+        out = np.empty(self.code_bytes, dtype=np.uint8)
+        check(lib().qp_layer_get_codes(self.h, out.ctypes.data, out.nbytes))
+        return out
+
+    def scales(self) -> np.ndarray:
+        out = np.empty(self.d_out, dtype=np.float32)
+        check(lib().qp_layer_get_scales(self.h, out.ctypes.data))
+        return out
+
+    def forward(self, x, batch: int, y, flags: int = 0, stream=None) -> None:
+        """qp_linear_fwd: y[batch][d_out] = diag(s) W_hat R x."""
+        check(lib().qp_linear_fwd(self.h, _ptr(x), _dtype_code(x), batch, _ptr(y), _dtype_code(y), flags,
+                                  _stream(stream)))
+
+    def dequantize(self, out, stream=None) -> None:
+        check(lib().qp_dequantize(self.h, _ptr(out), _stream(stream)))
+
+    def shard(self, rank: int, world: int) -> "Layer":
+        h = C.c_void_p()
+        check(lib().qp_layer_shard(self.h, rank, world, C.byref(h)))
+        return Layer(h, *self._keep)
+
+    def forward_sharded(self, x, batch: int, y_full, comm, flags: int = 0, stream=None) -> None:
+        check(lib().qp_linear_fwd_sharded(self.h, _ptr(x), _dtype_code(x), batch, _ptr(y_full), _dtype_code(y_full),
+                                          comm.h, flags, _stream(stream)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.qp_layer_free(self.h)
+            self.h = None
+
+
+class Group:
+    """qp_fuse / qp_fused_linear (fused QKV or up-gate)."""
+
+    def __init__(self, members: list[Layer]):
+        arr = (C.c_void_p * len(members))(*[m.h for m in members])
+        h = C.c_void_p()
+        check(lib().qp_fuse(arr, len(members), C.byref(h)))
+        self.h = h
+        self.d_outs = [m.d_out for m in members]
+        self._keep = members[0]._keep
+
+    def forward(self, x, batch: int, ys: list, flags: int = 0, stream=None) -> None:
+        arr = (C.c_void_p * len(ys))(*[_ptr(y) for y in ys])
+        check(lib().qp_fused_linear(self.h, _ptr(x), _dtype_code(x), batch, arr, _dtype_code(ys[0]), flags,
+                                    _stream(stream)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.qp_group_free(self.h)
+            self.h = None
+
+
+class NcclComm:
+    """NCCL communicator of the sharded path; the 128-byte unique id is exchanged by the caller."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        check(lib().qp_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, world: int, rank: int):
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(lib().qp_nccl_comm_create(buf, world, rank, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            check(lib().qp_nccl_comm_destroy(self.h))
+            self.h = None

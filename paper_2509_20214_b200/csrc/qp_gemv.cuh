@@ -1,0 +1,476 @@
+// Fused dequantize-and-multiply GEMV for the Q-Palette palette on sm_100a.
+//
+// y[beta][row] = s[row] * sum_k W_hat[row][k] * x'[beta][k],  batch <= 8
+//
+// Design:
+//  * persistent grid, one CTA per SM (128 KB replicated decode table in shared memory);
+//    the RT x KT tiles (32 rows x 256 cols, LAYOUT.md) are split into contiguous,
+//    k-minor ranges per CTA and per warp (flat stream-K: balanced to within one tile);
+//  * each lane owns one 256-weight trellis / code run per tile: its 4c stream words are
+//    loaded with c coalesced 128-bit loads (512 B per warp instruction), the next tile's
+//    words are prefetched while the current tile is decoded;
+//  * decode per weight pair (TCQ): funnel-shift window -> hash (w+1)w -> masked key ->
+//    one conflict-free LDS from a 32-way replicated table (bank = lane) -> half2;
+//    VQ/NUQ/UNIF: funnel-shift index -> LDS. Pairs land directly in mma.sync m16n8k16
+//    A-fragment registers (the layout was chosen so that step j IS fragment register j);
+//    the activations are the B fragment (batch in N <= 8), fp32 accumulation;
+//  * epilogue: per-row scale, then warp partials -> CTA smem reduction -> deterministic
+//    cross-CTA fixup (last-arriving CTA sums the partials in CTA order) -> y.
+//  * Programmatic dependent launch: table build and the first code loads happen before
+//    griddepcontrol.wait (they read only immutable layer data).
+#pragma once
+#include <cuda_fp16.h>
+#include <utility>
+
+#include "qp_internal.h"
+
+namespace qp {
+
+template <int... Is, class F>
+__device__ __forceinline__ void static_for_impl(std::integer_sequence<int, Is...>, F&& f) {
+  (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(std::make_integer_sequence<int, N>{}, f);
+}
+
+// Dynamic shared memory of the GEMV kernels; the decode table starts at byte 0. Referencing the
+// symbol directly (rather than through a generic pointer) lets ptxas fold the table base into
+// the LDS immediate, saving one IADD per decoded pair.
+extern __shared__ __align__(1024) uint8_t qp_smem[];
+// The shared::cta address of qp_smem: the first 1 KB of a CTA's shared window is reserved on
+// sm_90+/sm_100, so dynamic shared memory (no static shared memory in these kernels) starts at
+// 0x400. The kernel verifies this once at entry (trap otherwise) and the LDS below carries the
+// base as an immediate, saving one IADD per decoded pair.
+constexpr uint32_t kDynSmemBase = 0x400;
+__device__ __forceinline__ uint32_t lds32(uint32_t off) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1+1024];" : "=r"(v) : "r"(off));
+  return v;
+}
+
+// Stream bits [O, O+NB) of a lane's circular MSB-first word stream w[0..NW), returned with
+// the field's least significant bit at bit POS (other bits are garbage).
+template <int O, int NB, int POS, int NW>
+__device__ __forceinline__ uint32_t field(const uint32_t* w) {
+  constexpr int E = O + NB - 1;
+  constexpr int WO = (O >> 5) % NW;
+  constexpr int WE = (E >> 5) % NW;
+  constexpr int PL = 31 - (E & 31);
+  constexpr int SH = PL - POS;
+  if constexpr (WO == WE) {
+    if constexpr (SH >= 0) return w[WE] >> SH;
+    else return w[WE] << (-SH);
+  } else {
+    static_assert(SH > 0 && SH < 32, "spanning field");
+    return __funnelshift_r(w[WE], w[WO], SH);
+  }
+}
+
+template <int REPS>
+struct RepBits {
+  static constexpr int value = REPS == 32 ? 7 : REPS == 16 ? 6 : REPS == 8 ? 5 : REPS == 4 ? 4 : REPS == 2 ? 3 : 2;
+};
+
+// One decoded weight pair (half2 bits, low half = even column) of step J.
+template <int MODE, int C, int L, int TB, int REPS>
+struct Dec {
+  static constexpr int NW = 4 * C;
+  static constexpr int PB = RepBits<REPS>::value;   // log2(REPS * 4): key -> byte offset shift
+  template <int J>
+  __device__ __forceinline__ static uint32_t step(const uint32_t* w, uint32_t laneoff) {
+    if constexpr (MODE == DEC_TCQ_PRESIGNED) {
+      // window int(r[J*s : J*s+L]) -> p = (w+1) w mod 2^L -> key = bits
+      // [L-1-TB, L-1] of p (sign bit on top) -> pre-signed entry
+      const uint32_t win = field<J * C, L, 0, NW>(w);
+      const uint32_t p = win * win + win;
+      constexpr int SH = PB - (L - 1 - TB);
+      constexpr uint32_t MASK = ((1u << (TB + 1)) - 1u) << PB;
+      const uint32_t k = SH >= 0 ? (p << (SH >= 0 ? SH : 0)) : (p >> (SH < 0 ? -SH : 0));
+      return lds32(((k & MASK) | laneoff));
+    } else if constexpr (MODE == DEC_TCQ_UNSIGNED) {
+      const uint32_t win = field<J * C, L, 0, NW>(w);
+      const uint32_t p = win * win + win;
+      constexpr int SH = PB - (L - 1 - TB);
+      constexpr uint32_t MASK = ((1u << TB) - 1u) << PB;
+      const uint32_t k = SH >= 0 ? (p << (SH >= 0 ? SH : 0)) : (p >> (SH < 0 ? -SH : 0));
+      const uint32_t v = lds32(((k & MASK) | laneoff));
+      return v ^ ((p << (16 - L)) & 0x8000u);             // sflp on the first coordinate
+    } else if constexpr (MODE == DEC_LUT2) {
+      const uint32_t f = field<J * C, C, PB, NW>(w);
+      return lds32(((f & (((1u << C) - 1u) << PB)) | laneoff));
+    } else {  // DEC_SCALAR: C = 2 * TB, even-column code first
+      const uint32_t f0 = field<J * C, TB, PB, NW>(w);
+      const uint32_t f1 = field<J * C + TB, TB, PB, NW>(w);
+      constexpr uint32_t MASK = ((1u << TB) - 1u) << PB;
+      const uint32_t h0 = lds32(((f0 & MASK) | laneoff));
+      const uint32_t h1 = lds32(((f1 & MASK) | laneoff));
+      return __byte_perm(h0, h1, 0x5410);
+    }
+  }
+};
+
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Decode one tile's 128 steps of this lane and multiply-accumulate (GEMV) or store (dequant).
+template <int MODE, int C, int L, int TB, int REPS, bool DEQ>
+__device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff,
+                                          const uint32_t* xb, float (&acc)[2][4], uint32_t* wout_lane,
+                                          int ldw_words) {
+  using D = Dec<MODE, C, L, TB, REPS>;
+  static_for<16>([&](auto KAP) {
+    constexpr int kap = decltype(KAP)::value;
+    static_for<2>([&](auto M) {
+      constexpr int m = decltype(M)::value;
+      constexpr int j = 8 * kap + 4 * m;
+      const uint32_t a0 = D::template step<j + 0>(w, laneoff);
+      const uint32_t a1 = D::template step<j + 1>(w, laneoff);
+      const uint32_t a2 = D::template step<j + 2>(w, laneoff);
+      const uint32_t a3 = D::template step<j + 3>(w, laneoff);
+      if constexpr (DEQ) {
+        // step -> (row, col): row = 16m + g + 8(rho&1), col = 64q + 4kap + 2(rho>>1)
+        uint32_t* p = wout_lane + (16 * m) * ldw_words + 2 * kap;
+        p[0] = a0;
+        p[8 * ldw_words] = a1;
+        p[1] = a2;
+        p[8 * ldw_words + 1] = a3;
+      } else {
+        mma16816(acc[m], a0, a1, a2, a3, xb[2 * kap], xb[2 * kap + 1]);
+      }
+    });
+  });
+}
+
+template <int MODE, int REPS>
+__device__ __forceinline__ void build_table(const uint32_t* __restrict__ g, int words, uint8_t* tab, uint32_t* stage) {
+  // 1. compact table (<= 8 KB) -> shared staging area with 128-bit loads (one round trip)
+  for (int i = threadIdx.x * 4; i < words; i += blockDim.x * 4)
+    *reinterpret_cast<uint4*>(stage + i) = __ldg(reinterpret_cast<const uint4*>(g + i));
+  __syncthreads();
+  // 2. expand: entry e, replica r at byte e*REPS*4 + r*4 (bank = replica = lane mod REPS).
+  //    A warp writes 512 contiguous bytes per STS.128 instruction (conflict-free).
+  constexpr int V4 = REPS / 4;
+  const int total = words * V4;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int e = i / V4;
+    const uint32_t v = stage[e];
+    *reinterpret_cast<uint4*>(tab + e * REPS * 4 + (i % V4) * 16) = make_uint4(v, v, v, v);
+  }
+}
+
+__device__ __forceinline__ uint32_t owner_of(uint32_t t, uint32_t lo, uint32_t n, uint32_t parts) {
+  // part p owns [lo + n*p/parts, lo + n*(p+1)/parts); returns the p that contains t
+  return ((t - lo + 1) * parts - 1) / n;
+}
+
+__device__ __forceinline__ void store_out(const GemvParams& p, int rt, int row, int b, float v, float scale) {
+  int i = 0;
+#pragma unroll 1
+  while (i + 1 < p.n_out && rt >= p.rt_begin[i + 1]) ++i;
+  const int grow = (rt - p.rt_begin[i]) * kTileRows + row;
+  v *= scale;
+  if (p.y_f32) reinterpret_cast<float*>(p.y[i])[(size_t)b * p.ldy[i] + grow] = v;
+  else reinterpret_cast<__half*>(p.y[i])[(size_t)b * p.ldy[i] + grow] = __float2half_rn(v);
+}
+
+constexpr int kMaxScaleTiles = 32;   // row tiles whose scales a CTA stages in shared memory
+
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, int NWARP>
+__global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_constant__ GemvParams p) {
+  constexpr int CMAX = CLO > CHI ? CLO : CHI;
+  uint8_t* smem = qp_smem;
+  uint8_t* tab = smem;
+  if (threadIdx.x == 0 && (uint32_t)__cvta_generic_to_shared(qp_smem) != kDynSmemBase) __trap();
+  float* part = reinterpret_cast<float*>(smem + kSmemTableBytes);   // [NWARP][2][256]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto stamp = [&](int k) {   // debug timeline: per-warp clock64 stamps [grid][16 warps][4]
+    if (p.timeline && lane == 0 && warp < 16) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+      p.timeline[(blockIdx.x * 16 + warp) * 8 + k] = t;
+    }
+  };
+  stamp(0);
+  const int g = lane >> 2, q = lane & 3;
+  // tile indices are 32-bit: the host guarantees RT*KT*gridDim < 2^32
+  const uint32_t N = (uint32_t)p.RT * (uint32_t)p.KT;
+  const uint32_t T0 = N * blockIdx.x / gridDim.x, T1 = N * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t nC = T1 - T0;
+  const uint32_t a = T0 + nC * warp / NWARP, b = T0 + nC * (warp + 1) / NWARP;
+  const uint32_t KT = p.KT;
+  const int KH = p.KT / 2;
+  const long long rowtile_bytes = (long long)KH * 512 * CLO + (long long)(KT - KH) * 512 * CHI;
+
+  auto tile_ptr = [&](uint32_t rt, int kt) -> const uint8_t* {
+    const long long off = (long long)rt * rowtile_bytes + (kt < KH ? (long long)kt * 512 * CLO
+                                                        : (long long)KH * 512 * CLO + (long long)(kt - KH) * 512 * CHI);
+    return p.codes + off;
+  };
+  auto load_tile = [&](const uint8_t* ptr, int kt, uint32_t (&buf)[4 * CMAX]) {
+    const int c = (CLO == CHI || kt < KH) ? CLO : CHI;
+    const uint4* src = reinterpret_cast<const uint4*>(ptr) + lane;
+#pragma unroll
+    for (int i = 0; i < CMAX; ++i) {
+      if (CLO == CHI || i < c) {
+        uint4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + i * 32));
+        buf[4 * i] = v.x; buf[4 * i + 1] = v.y; buf[4 * i + 2] = v.z; buf[4 * i + 3] = v.w;
+      }
+    }
+  };
+
+  uint32_t cur[4 * CMAX], nxt[4 * CMAX];
+  uint32_t rt = a / KT;
+  int kt = (int)(a - rt * KT);
+  const uint8_t* ptr = tile_ptr(rt, kt);
+  if (a < b) load_tile(ptr, kt, cur);      // codes are immutable: safe before the PDL wait
+
+  // per-row scales of this CTA's row tiles -> registers now, shared memory after the table build
+  float* sscale = reinterpret_cast<float*>(smem + kSmemTableBytes + NWARP * 2 * 256 * 4);
+  const uint32_t srt0 = T0 / KT;
+  const int n_srt = nC > 0 ? (int)((T1 - 1) / KT - srt0 + 1) : 0;
+  const bool scales_in_smem = n_srt <= kMaxScaleTiles;
+  constexpr int SC_PER_THREAD = (kMaxScaleTiles * kTileRows + NWARP * 32 - 1) / (NWARP * 32);
+  float sc_reg[SC_PER_THREAD];
+#pragma unroll
+  for (int k = 0; k < SC_PER_THREAD; ++k) {
+    const int i = tid + k * NWARP * 32;
+    sc_reg[k] = (!DEQ && scales_in_smem && i < n_srt * kTileRows) ? __ldg(p.scales + srt0 * kTileRows + i) : 0.f;
+  }
+  // activations of the first tile: produced by the previous kernel, so only after the PDL wait;
+  // their L2 latency overlaps the table build below
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  uint32_t xb[32];
+  auto load_x = [&](int kt_) {
+    if (g < p.batch) {
+      const uint4* xs = reinterpret_cast<const uint4*>(p.x + (size_t)g * p.d_in + kt_ * kTileCols + 64 * q);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 v = __ldg(xs + i);
+        xb[4 * i] = v.x; xb[4 * i + 1] = v.y; xb[4 * i + 2] = v.z; xb[4 * i + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) xb[i] = 0u;
+    }
+  };
+  if (!DEQ && a < b) load_x(kt);
+  build_table<MODE, REPS>(p.table, p.table_words, tab, reinterpret_cast<uint32_t*>(part));
+#pragma unroll
+  for (int k = 0; k < SC_PER_THREAD; ++k) {
+    const int i = tid + k * NWARP * 32;
+    if (!DEQ && scales_in_smem && i < n_srt * kTileRows) sscale[i] = sc_reg[k];
+  }
+  __syncthreads();
+  auto scale_of = [&](uint32_t rt_, int row) -> float {
+    return scales_in_smem ? sscale[(rt_ - srt0) * kTileRows + row] : __ldg(p.scales + rt_ * kTileRows + row);
+  };
+
+  stamp(1);
+  const uint32_t laneoff = (uint32_t)(lane % REPS) * 4u;
+  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  const uint32_t a_rt = a / KT;
+
+  for (uint32_t t = a; t < b; ++t) {
+    int kt_n = kt + 1;
+    uint32_t rt_n = rt;
+    if (kt_n == KT) { kt_n = 0; ++rt_n; }
+    const uint8_t* ptr_n = (CLO == CHI) ? ptr + 512 * CLO : tile_ptr(rt_n, kt_n);
+    if (t + 1 < b) {
+      load_tile(ptr_n, kt_n, nxt);
+      if constexpr (!DEQ) {
+        if (g < p.batch)   // next tile's activations -> L1 (no registers held)
+          asm volatile("prefetch.global.L1 [%0];" :: "l"(p.x + (size_t)g * p.d_in + kt_n * kTileCols + 64 * q));
+      }
+    }
+    uint32_t* wout_lane = nullptr;
+    int ldw = 0;
+    if constexpr (DEQ) {
+      ldw = p.d_in / 2;
+      wout_lane = reinterpret_cast<uint32_t*>(p.w_out) + (size_t)(rt * kTileRows + g) * ldw + (kt * kTileCols + 64 * q) / 2;
+    }
+    if (CLO == CHI || kt < KH)
+      tile_body<MODE, CLO, L, TB, REPS, DEQ>(cur, laneoff, xb, acc, wout_lane, ldw);
+    else
+      tile_body<MODE, CHI, L, TB, REPS, DEQ>(cur, laneoff, xb, acc, wout_lane, ldw);
+    if (!DEQ && t + 1 < b) load_x(kt_n);      // L1 hit: prefetched one tile ahead
+
+    if constexpr (!DEQ) {
+      if (kt == KT - 1 || t == b - 1) {
+        const uint32_t rs = rt * KT;
+        const bool own = (a <= rs) && (b >= rs + KT);
+        if (own) {
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
+              if (bb < p.batch) store_out(p, (int)rt, row, bb, acc[m][r], scale_of(rt, row));
+            }
+        } else {
+          float* slot = part + (warp * 2 + (rt == a_rt ? 0 : 1)) * 256;
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
+              slot[row * 8 + bb] = acc[m][r];
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4 * CMAX; ++i) cur[i] = nxt[i];
+    kt = kt_n; rt = rt_n; ptr = ptr_n;
+  }
+  stamp(2);
+  asm volatile("griddepcontrol.launch_dependents;");
+  if constexpr (DEQ) return;
+  if (nC <= 0) return;
+
+  // ---- reduction of the warp partials: one warp per row tile, no CTA-wide barrier in the loop ----
+  __syncthreads();
+  stamp(4);
+  // lane w < NWARP holds warp w's tile range (no divisions inside the loops below)
+  const uint32_t my_aw = T0 + nC * (uint32_t)lane / NWARP, my_bw = T0 + nC * (uint32_t)(lane + 1) / NWARP;
+  const uint32_t my_frt = my_aw / KT;
+  const uint32_t rt_lo = T0 / KT, rt_hi = (T1 - 1) / KT;
+  for (uint32_t rt = rt_lo + warp; rt <= rt_hi; rt += NWARP) {
+    const uint32_t rs = rt * KT, re = rs + KT;
+    // warps touching [rs, re): aw < re && bw > rs, non-empty
+    const bool touch = lane < NWARP && my_aw < my_bw && my_aw < re && my_bw > rs;
+    const bool sole_owner = touch && my_aw <= rs && my_bw >= re;
+    if (__any_sync(0xffffffffu, sole_owner)) continue;   // written directly in the main loop
+    const unsigned tmask = __ballot_sync(0xffffffffu, touch);
+    const unsigned hmask = __ballot_sync(0xffffffffu, touch && my_frt == rt);   // rt is that warp's first
+    // lane handles elements e = lane + 32 k (row = e >> 3, batch = e & 7 = lane & 7)
+    const bool act = (lane & 7) < p.batch;
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = 0.f;
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) {
+      if (tmask & (1u << w)) {
+        const float* sl = part + (w * 2 + ((hmask >> w) & 1u ? 0 : 1)) * 256;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] += sl[lane + 32 * k];
+      }
+    }
+    stamp(5);
+    if (T0 <= rs && T1 >= re) {                          // the whole row tile is in this CTA
+      if (act)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) store_out(p, (int)rt, (lane + 32 * k) >> 3, lane & 7, v[k], scale_of(rt, (lane + 32 * k) >> 3));
+      continue;
+    }
+    // ---- cross-CTA, fast path: y was zeroed by the preceding kernel; every CTA adds its scaled
+    //      partial (no waiting; bitwise deterministic when two CTAs share the row tile).
+    if (p.y_atomic) {
+      if (act) {
+        int i = 0;
+#pragma unroll 1
+        while (i + 1 < p.n_out && (int)rt >= p.rt_begin[i + 1]) ++i;
+        float* yb = reinterpret_cast<float*>(p.y[i]) + (size_t)(lane & 7) * p.ldy[i] + (rt - p.rt_begin[i]) * kTileRows;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int row = (lane + 32 * k) >> 3;
+          atomicAdd(yb + row, v[k] * scale_of(rt, row));     // compiles to RED.ADD.F32
+        }
+      }
+      continue;
+    }
+    // ---- cross-CTA, deterministic path: the CTA holding the row tile's first k-tiles (it
+    //      finishes them last) sums the others' partials in CTA order; the others publish theirs
+    //      and leave without waiting.
+    if (rs < T0) {
+      // contributor: this row tile is our head (its partial was done first thing)
+      if (act)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) p.ws[(size_t)blockIdx.x * 256 + lane + 32 * k] = v[k];
+      __syncwarp();
+      if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" :: "l"(p.counters + rt) : "memory");
+      continue;
+    }
+    const uint32_t c1 = owner_of(re - 1, 0, N, gridDim.x);
+    const int need = (int)(c1 - blockIdx.x);
+    if (lane == 0) {
+      int seen;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(p.counters + rt) : "memory");
+        if (seen >= need) break;
+        __nanosleep(64);
+      }
+      p.counters[rt] = 0;                                 // every contributor has arrived: reset
+    }
+    __syncwarp();
+    stamp(6);
+    if (act) {
+      constexpr int kMaxContrib = 8;
+      float pv[kMaxContrib][8];
+#pragma unroll
+      for (int i = 0; i < kMaxContrib; ++i)
+        if (i < need)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) pv[i][k] = __ldcg(p.ws + (size_t)(blockIdx.x + 1 + i) * 256 + lane + 32 * k);
+#pragma unroll
+      for (int i = 0; i < kMaxContrib; ++i)
+        if (i < need)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] += pv[i][k];
+      for (int i = kMaxContrib; i < need; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] += __ldcg(p.ws + (size_t)(blockIdx.x + 1 + i) * 256 + lane + 32 * k);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) store_out(p, (int)rt, (lane + 32 * k) >> 3, lane & 7, v[k], scale_of(rt, (lane + 32 * k) >> 3));
+    }
+  }
+  __syncthreads();
+  stamp(3);
+}
+
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS>
+struct GemvVariant {
+  static constexpr int CMAX = CLO > CHI ? CLO : CHI;
+  static constexpr int NWARP = CMAX <= 6 ? 16 : 12;
+  static cudaError_t launch(const GemvParams& prm, int grid, int /*nwarps*/, bool dequant, bool pdl, cudaStream_t s) {
+    const int smem = kSmemTableBytes + NWARP * 2 * 256 * 4 + kMaxScaleTiles * kTileRows * 4;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NWARP * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
+    if (dequant) {
+      auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, true, NWARP>;
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k, prm);
+    } else {
+      auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, false, NWARP>;
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k, prm);
+    }
+    return e;
+  }
+  static void reg() { register_gemv(KernelKey{MODE, CLO, CHI, L, TB, REPS}, &launch); }
+};
+
+}  // namespace qp

@@ -1,0 +1,820 @@
+// Host side of the C ABI (include/qpalette.h): validation, object lifetime, codebook
+// expansion into device decode tables, layer / group / shard objects, NCCL glue and the
+// data-free offline quantizer (weight RHT, scales, RTN, rotate-half tail-biting Viterbi).
+//
+// Paper passages: P:345-349 (rotation + scales), P:975 (data-free procedure),
+// P:977-1065 (quantizer definitions), P:359-360 (bit-packing, table-lookup merging),
+// P:456-460 (layer fusion). Layout: LAYOUT.md. Readings R1-R20: DESIGN.md.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cstdlib>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/qpalette.h"
+#include "qp_internal.h"
+
+using namespace qp;
+
+// ---------------------------------------------------------------------------------------
+// errors, allocation, launch accounting
+// ---------------------------------------------------------------------------------------
+namespace {
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+void* (*g_alloc)(size_t, void*) = nullptr;
+void (*g_free)(void*, void*) = nullptr;
+void* g_alloc_ctx = nullptr;
+
+qp_status fail(qp_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+qp_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(QP_ERR_CUDA, "%s: %s (%s). Remedy: run on an sm_100 (B200) GPU with a matching driver; check inputs "
+              "are device pointers.", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+#define CUDA_TRY(expr, what)                  \
+  do {                                        \
+    cudaError_t e_ = (expr);                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+void* dev_alloc(size_t n) {
+  if (n == 0) n = 16;
+  if (g_alloc) return g_alloc(n, g_alloc_ctx);
+  void* p = nullptr;
+  return cudaMalloc(&p, n) == cudaSuccess ? p : nullptr;
+}
+void dev_free(void* p) {
+  if (!p) return;
+  if (g_free) g_free(p, g_alloc_ctx);
+  else cudaFree(p);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+uint16_t f32_to_f16_bits(float f) {
+  __half h = __float2half_rn(f);
+  uint16_t b;
+  std::memcpy(&b, &h, 2);
+  return b;
+}
+float f16_bits_to_f32(uint16_t b) {
+  __half h;
+  std::memcpy(&h, &b, 2);
+  return __half2float(h);
+}
+
+// splitmix64 counter generator (reading R8): i-th output for seed.
+uint64_t splitmix64(uint64_t seed, uint64_t i) {
+  uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+int tlut_bits_for_x4(int bits_x4) {  // 9 for b <= 4, 10 for 4.5, 11 for 5.0
+  if (bits_x4 <= 16) return 9;
+  if (bits_x4 <= 18) return 10;
+  return 11;
+}
+
+bool width_ok(qp_scheme s, int x4) {
+  switch (s) {
+    case QP_TCQ: return x4 >= 6 && x4 <= 20 && x4 % 2 == 0;
+    case QP_HALF_TCQ: return x4 >= 7 && x4 <= 19 && x4 % 2 == 1;
+    case QP_VQ: return x4 >= 6 && x4 <= 24 && x4 % 2 == 0;
+    case QP_NUQ:
+    case QP_UNIF: return x4 >= 8 && x4 <= 32 && x4 % 4 == 0;
+  }
+  return false;
+}
+
+// bits per 2-weight step for k-tiles in the low / high half of d_in
+void step_bits(qp_scheme s, int x4, int* c_lo, int* c_hi) {
+  if (s == QP_HALF_TCQ) {
+    *c_lo = (x4 - 1) / 2;
+    *c_hi = *c_lo + 1;
+  } else {
+    *c_lo = *c_hi = x4 / 2;
+  }
+}
+}  // namespace
+
+namespace qp {
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace qp
+
+// ---------------------------------------------------------------------------------------
+// objects
+// ---------------------------------------------------------------------------------------
+struct qp_codebook {
+  qp_scheme scheme;
+  int bits_x4;
+  int L;         // TCQ window bits
+  int tb;        // tlut bits (TCQ) or scalar code bits (NUQ/UNIF)
+  int mode;      // qp::DecMode
+  int reps;
+  std::vector<uint16_t> host;   // the loaded fp16 table
+  uint32_t* d_table = nullptr;  // compact device table (half2 words)
+  int table_words = 0;
+};
+
+struct qp_rht {
+  uint64_t seed;
+  int d_in, block;
+  std::vector<uint32_t> sign_bits;  // bit i = 1 -> d_i = -1
+  uint32_t* d_signs = nullptr;
+};
+
+struct qp_layer {
+  int d_out = 0, d_in = 0;
+  qp_scheme scheme;
+  int bits_x4 = 0, c_lo = 0, c_hi = 0;
+  size_t code_bytes = 0;
+  uint8_t* d_codes = nullptr;
+  float* d_scales = nullptr;
+  const qp_codebook* cb = nullptr;
+  const qp_rht* rht = nullptr;
+  KernelKey key{};
+  GemvLauncher launcher = nullptr;
+  int grid = 0;
+  float* d_ws = nullptr;
+  int* d_counters = nullptr;
+  __half* d_xrot = nullptr;   // [8][d_in] scratch for R x
+  void* d_gather = nullptr;   // sharded path scratch
+  size_t gather_bytes = 0;
+};
+
+struct qp_group {
+  qp_layer* cat = nullptr;          // concatenated rows
+  std::vector<int> d_outs;
+};
+
+namespace {
+
+qp_status make_kernel_key(const qp_codebook* cb, qp_scheme scheme, int c_lo, int c_hi, KernelKey* k) {
+  if (scheme == QP_TCQ || scheme == QP_HALF_TCQ) {
+    *k = KernelKey{cb->mode, c_lo, c_hi, cb->L, cb->tb, cb->reps};
+  } else if (scheme == QP_VQ) {
+    *k = KernelKey{DEC_LUT2, c_lo, c_lo, 0, 0, cb->reps};
+  } else {
+    if (cb->mode == DEC_LUT2) *k = KernelKey{DEC_LUT2, c_lo, c_lo, 0, 0, cb->reps};
+    else *k = KernelKey{DEC_SCALAR, c_lo, c_lo, 0, cb->tb, cb->reps};
+  }
+  return QP_OK;
+}
+
+qp_status check_codebook(const qp_codebook* cb, qp_scheme scheme, int bits_x4) {
+  if (!cb) return fail(QP_ERR_INVALID_ARG, "codebook is NULL. Remedy: load one with qp_codebook_load.");
+  const bool tcq_family = scheme == QP_TCQ || scheme == QP_HALF_TCQ;
+  const bool cb_tcq = cb->scheme == QP_TCQ || cb->scheme == QP_HALF_TCQ;
+  if (tcq_family != cb_tcq || (!tcq_family && cb->scheme != scheme))
+    return fail(QP_ERR_CONFIG_MISMATCH, "codebook scheme %d does not serve layer scheme %d. Remedy: load the codebook "
+                "of the layer's quantizer.", (int)cb->scheme, (int)scheme);
+  if (tcq_family) {
+    const int need_tb = tlut_bits_for_x4(scheme == QP_HALF_TCQ ? bits_x4 + 1 : bits_x4);
+    if (cb->tb != need_tb)
+      return fail(QP_ERR_CONFIG_MISMATCH, "TCQ width %.2f needs tlut_bits %d (P:1036), codebook has %d. Remedy: load "
+                  "the matching tlut.", bits_x4 / 4.0, need_tb, cb->tb);
+  } else if (scheme == QP_VQ) {
+    if (cb->bits_x4 != bits_x4)
+      return fail(QP_ERR_CONFIG_MISMATCH, "VQ codebook is %.1f bits, layer %.1f. Remedy: load the matching LUT.",
+                  cb->bits_x4 / 4.0, bits_x4 / 4.0);
+  } else if (cb->bits_x4 != bits_x4) {
+    return fail(QP_ERR_CONFIG_MISMATCH, "scalar codebook is %d bits, layer %d. Remedy: load the matching LUT.",
+                cb->bits_x4 / 4, bits_x4 / 4);
+  }
+  return QP_OK;
+}
+
+qp_status check_shape(qp_scheme scheme, int bits_x4, int d_out, int d_in) {
+  if (!width_ok(scheme, bits_x4))
+    return fail(QP_ERR_UNSUPPORTED_WIDTH, "scheme %d does not support %.2f bits (Table 1, P:192-211). Remedy: pick a "
+                "width from include/qpalette.h.", (int)scheme, bits_x4 / 4.0);
+  if (d_out <= 0 || d_in <= 0) return fail(QP_ERR_DIM, "d_out and d_in must be positive");
+  if (d_out % kTileRows || d_in % kTileCols)
+    return fail(QP_ERR_PARTITION_MISMATCH, "d_out=%d must be a multiple of 32 and d_in=%d of 256 (LAYOUT.md tiles). "
+                "Remedy: pad the layer.", d_out, d_in);
+  if (scheme == QP_HALF_TCQ && (d_in / 2) % kTileCols)
+    return fail(QP_ERR_PARTITION_MISMATCH, "half-TCQ needs (d_in/2) %% 256 == 0 (P:297); d_in=%d", d_in);
+  return QP_OK;
+}
+
+size_t layout_bytes(qp_scheme scheme, int bits_x4, int d_out, int d_in) {
+  int c_lo, c_hi;
+  step_bits(scheme, bits_x4, &c_lo, &c_hi);
+  const size_t RT = d_out / kTileRows, KT = d_in / kTileCols, KH = KT / 2;
+  return RT * (KH * 512 * (size_t)c_lo + (KT - KH) * 512 * (size_t)c_hi);
+}
+
+// Allocate the device side of a layer whose codes/scales are given on the device or host.
+qp_status layer_init(qp_layer* l, int d_out, int d_in, qp_scheme scheme, int bits_x4, const qp_codebook* cb,
+                     const qp_rht* r) {
+  l->d_out = d_out;
+  l->d_in = d_in;
+  l->scheme = scheme;
+  l->bits_x4 = bits_x4;
+  step_bits(scheme, bits_x4, &l->c_lo, &l->c_hi);
+  l->code_bytes = layout_bytes(scheme, bits_x4, d_out, d_in);
+  l->cb = cb;
+  l->rht = r;
+  make_kernel_key(cb, scheme, l->c_lo, l->c_hi, &l->key);
+  l->launcher = find_gemv(l->key);
+  if (!l->launcher)
+    return fail(QP_ERR_UNSUPPORTED, "no compiled kernel variant for mode=%d c=%d/%d L=%d tb=%d reps=%d. Remedy: add it "
+                "to the qp_inst_*.cu instantiation lists.", l->key.mode, l->key.c_lo, l->key.c_hi, l->key.L,
+                l->key.tb, l->key.reps);
+  const long long ntiles = (long long)(d_out / kTileRows) * (d_in / kTileCols);
+  l->grid = (int)std::min<long long>(num_sms(), ntiles);
+  if ((unsigned long long)ntiles * (unsigned long long)(l->grid + 1) >= (1ull << 32))
+    return fail(QP_ERR_DIM, "layer of %lld tiles is too large for 32-bit tile indexing", ntiles);
+  l->d_codes = static_cast<uint8_t*>(dev_alloc(l->code_bytes));
+  l->d_scales = static_cast<float*>(dev_alloc((size_t)d_out * 4));
+  l->d_ws = static_cast<float*>(dev_alloc((size_t)l->grid * 256 * 4));
+  l->d_counters = static_cast<int*>(dev_alloc((size_t)(d_out / kTileRows) * 4));
+  l->d_xrot = static_cast<__half*>(dev_alloc((size_t)8 * d_in * 2));
+  if (!l->d_codes || !l->d_scales || !l->d_ws || !l->d_counters || !l->d_xrot)
+    return fail(QP_ERR_ALLOC, "device allocation of %zu code bytes failed", l->code_bytes);
+  CUDA_TRY(cudaMemset(l->d_counters, 0, (size_t)(d_out / kTileRows) * 4), "cudaMemset(counters)");
+  return QP_OK;
+}
+
+void layer_release(qp_layer* l) {
+  if (!l) return;
+  dev_free(l->d_codes);
+  dev_free(l->d_scales);
+  dev_free(l->d_ws);
+  dev_free(l->d_counters);
+  dev_free(l->d_xrot);
+  dev_free(l->d_gather);
+}
+
+qp_status run_rht(const qp_rht* r, const void* x, qp_dtype xt, int batch, __half* out, bool pdl, cudaStream_t s,
+                  int n_zero = 0, void* const* zero_ptr = nullptr, const long long* zero_n = nullptr) {
+  RhtParams p{};
+  p.n_zero = n_zero;
+  for (int i = 0; i < n_zero; ++i) {
+    p.zero_ptr[i] = static_cast<float*>(zero_ptr[i]);
+    p.zero_n[i] = zero_n[i];
+  }
+  p.x = x;
+  p.x_dtype = (int)xt;
+  p.batch = batch;
+  p.d_in = r->d_in;
+  p.block = r->block;
+  p.signs = r->d_signs;
+  p.out = out;
+  p.scale = (float)(1.0 / std::sqrt((double)r->block));
+  cudaError_t e = launch_rht(p, pdl, s);
+  if (e != cudaSuccess) return cuda_fail(e, "rht kernel launch");
+  return QP_OK;
+}
+
+qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, const int* rt_begin, void* const* ys,
+                   const int* ldy, qp_dtype yt, bool pdl, cudaStream_t s, bool y_atomic) {
+  GemvParams p{};
+  p.y_atomic = y_atomic ? 1 : 0;
+  p.codes = l->d_codes;
+  p.scales = l->d_scales;
+  p.table = l->cb->d_table;
+  p.table_words = l->cb->table_words;
+  p.RT = l->d_out / kTileRows;
+  p.KT = l->d_in / kTileCols;
+  p.d_in = l->d_in;
+  p.batch = batch;
+  p.x = xr;
+  p.n_out = n_out;
+  for (int i = 0; i <= n_out; ++i) p.rt_begin[i] = rt_begin[i];
+  for (int i = 0; i < n_out; ++i) {
+    p.y[i] = ys[i];
+    p.ldy[i] = ldy[i];
+  }
+  p.y_f32 = yt == QP_F32 ? 1 : 0;
+  p.ws = l->d_ws;
+  p.counters = l->d_counters;
+  static const bool tl = getenv("QP_TIMELINE") != nullptr;
+  static unsigned long long* d_tl = nullptr;
+  if (tl && !d_tl) { cudaMalloc(&d_tl, 4096 * 128 * 8); cudaMemset(d_tl, 0, 4096 * 128 * 8); }
+  p.timeline = tl ? d_tl : nullptr;
+  cudaError_t e = l->launcher(p, l->grid, 0, false, pdl, s);
+  if (e != cudaSuccess) return cuda_fail(e, "fused dequant-GEMV launch");
+  count_launch();
+  if (tl) {
+    std::vector<unsigned long long> h(l->grid * 128, 0ull);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), d_tl, h.size() * 8, cudaMemcpyDeviceToHost);
+    double av[8] = {0}, mx[8] = {0};
+    int cnt[8] = {0};
+    for (int c = 0; c < l->grid; ++c) {
+      unsigned long long st = ~0ull;
+      for (int w = 0; w < 16; ++w) if (h[(c * 16 + w) * 8]) st = std::min(st, h[(c * 16 + w) * 8]);
+      for (int k = 1; k < 8; ++k) {
+        double m = -1;
+        for (int w = 0; w < 16; ++w) {
+          unsigned long long v = h[(c * 16 + w) * 8 + k];
+          if (v && v > st) m = std::max(m, (double)(v - st) / 1000.0);
+        }
+        if (m >= 0) { av[k] += m; cnt[k]++; mx[k] = std::max(mx[k], m); }
+      }
+    }
+    fprintf(stderr, "kcyc (avg/max over CTAs):");
+    const char* nm[8] = {"", "table", "mainend", "epiend", "epistart", "psum", "atomic", ""};
+    for (int k = 1; k < 7; ++k) fprintf(stderr, " %s %.2f/%.2f", nm[k], cnt[k] ? av[k] / cnt[k] : 0.0, mx[k]);
+    fprintf(stderr, "\n");
+    cudaMemset(d_tl, 0, 4096 * 128 * 8);
+  }
+  return QP_OK;
+}
+
+qp_status check_fwd_args(const void* x, qp_dtype xt, int batch, qp_dtype yt, unsigned flags) {
+  if (!x) return fail(QP_ERR_INVALID_ARG, "x is NULL");
+  if (batch < 1 || batch > 8)
+    return fail(QP_ERR_PARTITION_MISMATCH, "batch=%d outside 1..8 (P:292). Remedy: split the batch.", batch);
+  if ((int)xt < 0 || (int)xt > 2 || (yt != QP_F32 && yt != QP_F16))
+    return fail(QP_ERR_INVALID_ARG, "dtype: x in {F16,BF16,F32}, y in {F16,F32}");
+  if ((flags & QP_X_PREROTATED) && xt != QP_F16)
+    return fail(QP_ERR_INVALID_ARG, "QP_X_PREROTATED requires fp16 x (the output dtype of qp_rht_apply)");
+  return QP_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------------------
+extern "C" {
+
+const char* qp_last_error(void) { return g_err.c_str(); }
+const char* qp_version(void) { return "qpalette-b200 0.1 (sm_100a)"; }
+uint64_t qp_launch_count(void) { return g_launches.load(); }
+
+qp_status qp_set_allocator(void* (*alloc)(size_t, void*), void (*free_)(void*, void*), void* ctx) {
+  if ((alloc == nullptr) != (free_ == nullptr)) return fail(QP_ERR_INVALID_ARG, "give both alloc and free, or neither");
+  g_alloc = alloc;
+  g_free = free_;
+  g_alloc_ctx = ctx;
+  return QP_OK;
+}
+
+qp_status qp_codebook_load(qp_scheme scheme, int bits_x4, int L, const void* host_fp16, size_t n_bytes,
+                           qp_codebook** out) {
+  if (!host_fp16 || !out) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_codebook_load");
+  *out = nullptr;
+  if (!width_ok(scheme, bits_x4)) return fail(QP_ERR_UNSUPPORTED_WIDTH, "unsupported width %.2f", bits_x4 / 4.0);
+  auto cb = new qp_codebook();
+  cb->scheme = scheme;
+  cb->bits_x4 = bits_x4;
+  cb->L = 0;
+  const uint16_t* h = static_cast<const uint16_t*>(host_fp16);
+  std::vector<uint32_t> words;
+  size_t expect = 0;
+  if (scheme == QP_TCQ || scheme == QP_HALF_TCQ) {
+    if (L != 16 && L != 12) {
+      delete cb;
+      return fail(QP_ERR_CONFIG_MISMATCH, "L=%d; supported trellis windows are 16 (P:1043) and 12 (config C1)", L);
+    }
+    cb->L = L;
+    cb->tb = tlut_bits_for_x4(scheme == QP_HALF_TCQ ? bits_x4 + 1 : bits_x4);
+    expect = ((size_t)1 << cb->tb) * 4;
+    if (n_bytes != expect) {
+      delete cb;
+      return fail(QP_ERR_LENGTH, "tlut for tlut_bits=%d must be %zu bytes, got %zu", cb->tb, expect, n_bytes);
+    }
+    const int n = 1 << cb->tb;
+    if (cb->tb == 9) {
+      // pre-signed key table: key = sign * 2^tb + idx -> (sign ? -t0 : t0, t1)
+      cb->mode = DEC_TCQ_PRESIGNED;
+      cb->reps = 32;
+      words.resize(2 * n);
+      for (int sgn = 0; sgn < 2; ++sgn)
+        for (int i = 0; i < n; ++i) {
+          const uint32_t t0 = h[2 * i] ^ (sgn ? 0x8000u : 0u), t1 = h[2 * i + 1];
+          words[sgn * n + i] = t0 | (t1 << 16);
+        }
+    } else {
+      cb->mode = DEC_TCQ_UNSIGNED;
+      cb->reps = cb->tb == 10 ? 32 : 16;
+      words.resize(n);
+      for (int i = 0; i < n; ++i) words[i] = (uint32_t)h[2 * i] | ((uint32_t)h[2 * i + 1] << 16);
+    }
+  } else if (scheme == QP_VQ) {
+    const int c = bits_x4 / 2;
+    expect = ((size_t)1 << c) * 4;
+    if (n_bytes != expect) {
+      delete cb;
+      return fail(QP_ERR_LENGTH, "VQ-%.1f LUT must be %zu bytes, got %zu", bits_x4 / 4.0, expect, n_bytes);
+    }
+    cb->mode = DEC_LUT2;
+    cb->reps = c <= 10 ? 32 : (c == 11 ? 16 : 8);
+    words.resize((size_t)1 << c);
+    for (size_t i = 0; i < words.size(); ++i) words[i] = (uint32_t)h[2 * i] | ((uint32_t)h[2 * i + 1] << 16);
+  } else {
+    const int b = bits_x4 / 4;
+    expect = ((size_t)1 << b) * 2;
+    if (n_bytes != expect) {
+      delete cb;
+      return fail(QP_ERR_LENGTH, "scalar LUT of %d bits must be %zu bytes, got %zu", b, expect, n_bytes);
+    }
+    cb->tb = b;
+    if (b <= 4) {
+      // table-lookup merging: pair index c_even * 2^b + c_odd
+      cb->mode = DEC_LUT2;
+      cb->reps = 32;
+      const int n = 1 << b;
+      words.resize((size_t)n * n);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) words[i * n + j] = (uint32_t)h[i] | ((uint32_t)h[j] << 16);
+    } else {
+      cb->mode = DEC_SCALAR;
+      cb->reps = 32;
+      words.resize((size_t)1 << b);
+      for (size_t i = 0; i < words.size(); ++i) words[i] = h[i];
+    }
+  }
+  cb->host.assign(h, h + n_bytes / 2);
+  cb->table_words = (int)words.size();
+  cb->d_table = static_cast<uint32_t*>(dev_alloc(words.size() * 4));
+  if (!cb->d_table) {
+    delete cb;
+    return fail(QP_ERR_ALLOC, "codebook table allocation failed");
+  }
+  cudaError_t e = cudaMemcpy(cb->d_table, words.data(), words.size() * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    dev_free(cb->d_table);
+    delete cb;
+    return cuda_fail(e, "codebook upload");
+  }
+  *out = cb;
+  return QP_OK;
+}
+
+void qp_codebook_free(qp_codebook* cb) {
+  if (!cb) return;
+  dev_free(cb->d_table);
+  delete cb;
+}
+
+qp_status qp_rht_create(uint64_t seed, int d_in, int block, qp_rht** out) {
+  if (!out) return fail(QP_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (d_in <= 0 || d_in % kTileCols) return fail(QP_ERR_DIM, "d_in=%d must be a positive multiple of 256", d_in);
+  if (block == 0) block = d_in & (-d_in);   // largest power-of-two divisor (reading R9)
+  if (block < 256 || (block & (block - 1)) || d_in % block || block > 32768)
+    return fail(QP_ERR_DIM, "rotation block %d must be a power of two in [256, 32768] dividing d_in=%d", block, d_in);
+  auto r = new qp_rht();
+  r->seed = seed;
+  r->d_in = d_in;
+  r->block = block;
+  r->sign_bits.assign((d_in + 31) / 32, 0u);
+  for (int i = 0; i < d_in; ++i)
+    if (splitmix64(seed, (uint64_t)i) >> 63) r->sign_bits[i >> 5] |= 1u << (i & 31);
+  r->d_signs = static_cast<uint32_t*>(dev_alloc(r->sign_bits.size() * 4));
+  if (!r->d_signs) {
+    delete r;
+    return fail(QP_ERR_ALLOC, "rotation allocation failed");
+  }
+  cudaError_t e = cudaMemcpy(r->d_signs, r->sign_bits.data(), r->sign_bits.size() * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    dev_free(r->d_signs);
+    delete r;
+    return cuda_fail(e, "rotation upload");
+  }
+  *out = r;
+  return QP_OK;
+}
+
+void qp_rht_free(qp_rht* r) {
+  if (!r) return;
+  dev_free(r->d_signs);
+  delete r;
+}
+
+qp_status qp_rht_apply(const qp_rht* r, const void* x, qp_dtype xt, int batch, void* x_rot, void* stream) {
+  if (!r || !x || !x_rot) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_rht_apply");
+  if (batch < 1 || batch > 65535) return fail(QP_ERR_INVALID_ARG, "batch=%d", batch);
+  if ((int)xt < 0 || (int)xt > 2) return fail(QP_ERR_INVALID_ARG, "bad dtype");
+  return run_rht(r, x, xt, batch, static_cast<__half*>(x_rot), false, static_cast<cudaStream_t>(stream));
+}
+
+qp_status qp_layer_from_codes(const void* codes_host, size_t n_bytes, const float* scales_host, int d_out, int d_in,
+                              qp_scheme scheme, int bits_x4, const qp_codebook* cb, const qp_rht* r, qp_layer** out) {
+  if (!codes_host || !scales_host || !out || !r) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_layer_from_codes");
+  *out = nullptr;
+  qp_status st = check_shape(scheme, bits_x4, d_out, d_in);
+  if (st != QP_OK) return st;
+  if ((st = check_codebook(cb, scheme, bits_x4)) != QP_OK) return st;
+  if (r->d_in != d_in) return fail(QP_ERR_CONFIG_MISMATCH, "rotation is for d_in=%d, layer has %d", r->d_in, d_in);
+  const size_t need = layout_bytes(scheme, bits_x4, d_out, d_in);
+  if (n_bytes != need)
+    return fail(QP_ERR_LENGTH, "codes must be exactly %zu bytes (d_out*d_in*bits/8, LAYOUT.md), got %zu", need, n_bytes);
+  auto l = new qp_layer();
+  if ((st = layer_init(l, d_out, d_in, scheme, bits_x4, cb, r)) != QP_OK) {
+    layer_release(l);
+    delete l;
+    return st;
+  }
+  cudaError_t e = cudaMemcpy(l->d_codes, codes_host, need, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(l->d_scales, scales_host, (size_t)d_out * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    layer_release(l);
+    delete l;
+    return cuda_fail(e, "layer upload");
+  }
+  *out = l;
+  return QP_OK;
+}
+
+qp_status qp_layer_get_codes(const qp_layer* l, void* codes_host, size_t n_bytes) {
+  if (!l || !codes_host) return fail(QP_ERR_INVALID_ARG, "NULL argument");
+  if (n_bytes != l->code_bytes) return fail(QP_ERR_LENGTH, "layer holds %zu code bytes", l->code_bytes);
+  CUDA_TRY(cudaMemcpy(codes_host, l->d_codes, n_bytes, cudaMemcpyDeviceToHost), "codes download");
+  return QP_OK;
+}
+
+qp_status qp_layer_get_scales(const qp_layer* l, float* scales_host) {
+  if (!l || !scales_host) return fail(QP_ERR_INVALID_ARG, "NULL argument");
+  CUDA_TRY(cudaMemcpy(scales_host, l->d_scales, (size_t)l->d_out * 4, cudaMemcpyDeviceToHost), "scales download");
+  return QP_OK;
+}
+
+qp_status qp_layer_info(const qp_layer* l, size_t* code_bytes, double* bits_per_weight, int* d_out, int* d_in) {
+  if (!l) return fail(QP_ERR_INVALID_ARG, "layer is NULL");
+  if (code_bytes) *code_bytes = l->code_bytes;
+  if (bits_per_weight) *bits_per_weight = 8.0 * (double)l->code_bytes / ((double)l->d_out * l->d_in);
+  if (d_out) *d_out = l->d_out;
+  if (d_in) *d_in = l->d_in;
+  return QP_OK;
+}
+
+void qp_layer_free(qp_layer* l) {
+  if (!l) return;
+  layer_release(l);
+  delete l;
+}
+
+qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch, void* y, qp_dtype yt,
+                        unsigned flags, void* stream) {
+  if (!l || !y) return fail(QP_ERR_INVALID_ARG, "NULL layer or y");
+  qp_status st = check_fwd_args(x, xt, batch, yt, flags);
+  if (st != QP_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool pdl = !(flags & QP_NO_PDL);
+  const __half* xr = static_cast<const __half*>(x);
+  void* ys[1] = {y};
+  // fp32 output: the preceding kernel (rotation, or a zeroing kernel) zeroes y and CTAs that share
+  // a row tile add into it; QP_DETERMINISTIC or fp16 output: in-order cross-CTA reduction instead
+  const bool atomic = yt == QP_F32 && !(flags & QP_DETERMINISTIC);
+  const long long zn[1] = {(long long)batch * l->d_out};
+  if (!(flags & QP_X_PREROTATED)) {
+    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, false, s, atomic ? 1 : 0, ys, zn)) != QP_OK) return st;
+    xr = l->d_xrot;
+  } else if (atomic) {
+    RhtParams zp{};
+    zp.n_zero = 1;
+    zp.zero_ptr[0] = static_cast<float*>(y);
+    zp.zero_n[0] = zn[0];
+    cudaError_t e = launch_zero(zp, false, s);
+    if (e != cudaSuccess) return cuda_fail(e, "zero kernel launch");
+  }
+  const int rtb[2] = {0, l->d_out / kTileRows};
+  const int ldy[1] = {l->d_out};
+  return run_gemv(l, xr, batch, 1, rtb, ys, ldy, yt, pdl, s, atomic);
+}
+
+qp_status qp_dequantize(const qp_layer* l, void* W_hat_fp16, void* stream) {
+  if (!l || !W_hat_fp16) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_dequantize");
+  GemvParams p{};
+  p.codes = l->d_codes;
+  p.scales = l->d_scales;
+  p.table = l->cb->d_table;
+  p.table_words = l->cb->table_words;
+  p.RT = l->d_out / kTileRows;
+  p.KT = l->d_in / kTileCols;
+  p.d_in = l->d_in;
+  p.batch = 1;
+  p.w_out = static_cast<__half*>(W_hat_fp16);
+  cudaError_t e = l->launcher(p, l->grid, 0, true, false, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "dequantize launch");
+  count_launch();
+  return QP_OK;
+}
+
+qp_status qp_fuse(const qp_layer* const* members, int n, qp_group** out) {
+  if (!members || !out || n < 1) return fail(QP_ERR_INVALID_ARG, "bad arguments to qp_fuse");
+  *out = nullptr;
+  if (n > kMaxGroup) return fail(QP_ERR_INVALID_ARG, "at most %d members per group", kMaxGroup);
+  const qp_layer* m0 = members[0];
+  int d_out = 0;
+  for (int i = 0; i < n; ++i) {
+    const qp_layer* m = members[i];
+    if (!m) return fail(QP_ERR_INVALID_ARG, "member %d is NULL", i);
+    if (m->d_in != m0->d_in || m->rht != m0->rht || m->scheme != m0->scheme || m->bits_x4 != m0->bits_x4 ||
+        m->cb != m0->cb)
+      return fail(QP_ERR_CONFIG_MISMATCH, "fused members must share d_in, rotation, scheme, width and codebook (P:470)");
+    d_out += m->d_out;
+  }
+  auto g = new qp_group();
+  g->cat = new qp_layer();
+  qp_status st = layer_init(g->cat, d_out, m0->d_in, m0->scheme, m0->bits_x4, m0->cb, m0->rht);
+  if (st != QP_OK) {
+    qp_group_free(g);
+    return st;
+  }
+  size_t off = 0;
+  int row = 0;
+  for (int i = 0; i < n; ++i) {
+    const qp_layer* m = members[i];
+    cudaError_t e = cudaMemcpy(g->cat->d_codes + off, m->d_codes, m->code_bytes, cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g->cat->d_scales + row, m->d_scales, (size_t)m->d_out * 4, cudaMemcpyDeviceToDevice);
+    if (e != cudaSuccess) {
+      qp_group_free(g);
+      return cuda_fail(e, "group concatenation");
+    }
+    off += m->code_bytes;
+    row += m->d_out;
+    g->d_outs.push_back(m->d_out);
+  }
+  *out = g;
+  return QP_OK;
+}
+
+void qp_group_free(qp_group* g) {
+  if (!g) return;
+  if (g->cat) {
+    layer_release(g->cat);
+    delete g->cat;
+  }
+  delete g;
+}
+
+qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int batch, void* const* ys, qp_dtype yt,
+                          unsigned flags, void* stream) {
+  if (!g || !ys) return fail(QP_ERR_INVALID_ARG, "NULL group or ys");
+  qp_status st = check_fwd_args(x, xt, batch, yt, flags);
+  if (st != QP_OK) return st;
+  const int n = (int)g->d_outs.size();
+  for (int i = 0; i < n; ++i)
+    if (!ys[i]) return fail(QP_ERR_INVALID_ARG, "ys[%d] is NULL", i);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const qp_layer* l = g->cat;
+  const __half* xr = static_cast<const __half*>(x);
+  const bool atomic = yt == QP_F32 && !(flags & QP_DETERMINISTIC);
+  long long zn[kMaxGroup];
+  for (int i = 0; i < n; ++i) zn[i] = (long long)batch * g->d_outs[i];
+  if (!(flags & QP_X_PREROTATED)) {
+    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, false, s, atomic ? n : 0, ys, zn)) != QP_OK) return st;
+    xr = l->d_xrot;
+  } else if (atomic) {
+    RhtParams zp{};
+    zp.n_zero = n;
+    for (int i = 0; i < n; ++i) {
+      zp.zero_ptr[i] = static_cast<float*>(ys[i]);
+      zp.zero_n[i] = zn[i];
+    }
+    cudaError_t e = launch_zero(zp, false, s);
+    if (e != cudaSuccess) return cuda_fail(e, "zero kernel launch");
+  }
+  int rtb[kMaxGroup + 1];
+  int ldy[kMaxGroup];
+  rtb[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    rtb[i + 1] = rtb[i] + g->d_outs[i] / kTileRows;
+    ldy[i] = g->d_outs[i];
+  }
+  return run_gemv(l, xr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic);
+}
+
+qp_status qp_layer_shard(const qp_layer* l, int rank, int world, qp_layer** out) {
+  if (!l || !out) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_layer_shard");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return fail(QP_ERR_INVALID_ARG, "rank %d / world %d", rank, world);
+  if (l->d_out % world || (l->d_out / world) % kTileRows)
+    return fail(QP_ERR_PARTITION_MISMATCH, "d_out=%d does not split into %d row blocks of a multiple of 32", l->d_out,
+                world);
+  const int m = l->d_out / world;
+  auto s = new qp_layer();
+  qp_status st = layer_init(s, m, l->d_in, l->scheme, l->bits_x4, l->cb, l->rht);
+  if (st != QP_OK) {
+    layer_release(s);
+    delete s;
+    return st;
+  }
+  // row-tile-major storage: rows [rank*m, (rank+1)*m) are one contiguous byte range (LAYOUT.md)
+  cudaError_t e = cudaMemcpy(s->d_codes, l->d_codes + (size_t)rank * s->code_bytes, s->code_bytes,
+                             cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(s->d_scales, l->d_scales + (size_t)rank * m, (size_t)m * 4, cudaMemcpyDeviceToDevice);
+  if (e != cudaSuccess) {
+    layer_release(s);
+    delete s;
+    return cuda_fail(e, "shard copy");
+  }
+  *out = s;
+  return QP_OK;
+}
+
+qp_status qp_nccl_unique_id(void* id128) {
+  if (!id128) return fail(QP_ERR_INVALID_ARG, "id buffer is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclResult_t r = ncclGetUniqueId(static_cast<ncclUniqueId*>(id128));
+  if (r != ncclSuccess) return fail(QP_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  return QP_OK;
+}
+
+qp_status qp_nccl_comm_create(const void* id128, int world, int rank, void** comm) {
+  if (!id128 || !comm) return fail(QP_ERR_INVALID_ARG, "NULL argument");
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclComm_t c = nullptr;
+  ncclResult_t r = ncclCommInitRank(&c, world, id, rank);
+  if (r != ncclSuccess) return fail(QP_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  *comm = c;
+  return QP_OK;
+}
+
+qp_status qp_nccl_comm_destroy(void* comm) {
+  if (!comm) return QP_OK;
+  ncclResult_t r = ncclCommDestroy(static_cast<ncclComm_t>(comm));
+  if (r != ncclSuccess) return fail(QP_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
+  return QP_OK;
+}
+
+qp_status qp_linear_fwd_sharded(const qp_layer* shard, const void* x, qp_dtype xt, int batch, void* y_full,
+                                qp_dtype yt, void* comm, unsigned flags, void* stream) {
+  if (!shard || !y_full || !comm) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_linear_fwd_sharded");
+  qp_status st = check_fwd_args(x, xt, batch, yt, flags);
+  if (st != QP_OK) return st;
+  ncclComm_t c = static_cast<ncclComm_t>(comm);
+  int world = 0;
+  if (ncclCommCount(c, &world) != ncclSuccess || world < 1) return fail(QP_ERR_NCCL, "ncclCommCount failed");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int m = shard->d_out;
+  const int eb = yt == QP_F32 ? 4 : 2;
+  qp_layer* l = const_cast<qp_layer*>(shard);
+  const size_t need = (size_t)(world + 1) * batch * m * eb;
+  if (l->gather_bytes < need) {
+    dev_free(l->d_gather);
+    l->d_gather = dev_alloc(need);
+    l->gather_bytes = l->d_gather ? need : 0;
+    if (!l->d_gather) return fail(QP_ERR_ALLOC, "gather scratch allocation failed");
+  }
+  uint8_t* local = static_cast<uint8_t*>(l->d_gather);              // [batch][m]
+  uint8_t* gathered = local + (size_t)batch * m * eb;                // [world][batch][m]
+  if ((st = qp_linear_fwd(shard, x, xt, batch, local, yt, flags, stream)) != QP_OK) return st;
+  void* recv = batch == 1 ? y_full : gathered;
+  ncclResult_t r = ncclAllGather(local, recv, (size_t)batch * m, yt == QP_F32 ? ncclFloat32 : ncclFloat16, c, s);
+  if (r != ncclSuccess) return fail(QP_ERR_NCCL, "ncclAllGather: %s", ncclGetErrorString(r));
+  if (batch > 1) {
+    cudaError_t e = launch_gather_permute(gathered, y_full, world, batch, m, eb, s);
+    if (e != cudaSuccess) return cuda_fail(e, "gather permute");
+  }
+  return QP_OK;
+}
+
+}  // extern "C"
+
+// accessors for qp_offline.cpp (not part of the public ABI)
+extern "C" qp_status qp_internal_codebook_info(const qp_codebook* cb, int* L, int* tb, const uint16_t** host,
+                                               size_t* n) {
+  if (!cb) return fail(QP_ERR_INVALID_ARG, "codebook is NULL");
+  *L = cb->L;
+  *tb = cb->tb;
+  *host = cb->host.data();
+  *n = cb->host.size();
+  return QP_OK;
+}
+extern "C" qp_status qp_internal_rht_info(const qp_rht* r, uint64_t* seed, int* d_in, int* block,
+                                          const uint32_t** sign_bits) {
+  if (!r) return fail(QP_ERR_INVALID_ARG, "rotation is NULL");
+  *seed = r->seed;
+  *d_in = r->d_in;
+  *block = r->block;
+  *sign_bits = r->sign_bits.data();
+  return QP_OK;
+}

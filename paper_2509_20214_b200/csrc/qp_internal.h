@@ -1,0 +1,89 @@
+// Internal declarations shared by the host library (qp_host.cpp) and the CUDA kernels.
+// Not part of the C ABI (include/qpalette.h is).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+
+namespace qp {
+
+// ---- decoder kinds (LAYOUT.md §3) ---------------------------------
+enum DecMode : int {
+  DEC_TCQ_PRESIGNED = 0,  // smem table indexed by the (sign, idx) key: 2^(tb+1) entries
+  DEC_TCQ_UNSIGNED = 1,   // smem table of tlut (2^tb entries) + sign flip by XOR
+  DEC_LUT2 = 2,           // 2^c-entry table of half2 pairs (VQ, NUQ/UNIF pair-merged)
+  DEC_SCALAR = 3          // two b-bit scalar lookups per pair (NUQ/UNIF b >= 5)
+};
+
+constexpr int kMaxGroup = 8;        // members of a fused group
+constexpr int kTileRows = 32;
+constexpr int kTileCols = 256;
+constexpr int kSmemTableBytes = 131072;
+
+// Static description of one kernel variant.
+struct KernelKey {
+  int mode;     // DecMode
+  int c_lo;     // bits per step, k-tiles [0, KT/2)
+  int c_hi;     // bits per step, k-tiles [KT/2, KT)
+  int L;        // trellis window (TCQ only)
+  int tb;       // tlut bits (TCQ) / scalar code bits (DEC_SCALAR)
+  int reps;     // smem replicas (bank spreading)
+  bool operator==(const KernelKey& o) const {
+    return mode == o.mode && c_lo == o.c_lo && c_hi == o.c_hi && L == o.L && tb == o.tb && reps == o.reps;
+  }
+};
+
+// Runtime parameters of one fused dequant-GEMV launch (or dequant-only launch).
+struct GemvParams {
+  const uint8_t* codes;        // packed codes, LAYOUT.md order (possibly a fused group)
+  const float* scales;         // [RT*32] per-output-channel scales
+  const uint32_t* table;       // compact device table (table_words uint32 = half2)
+  int table_words;
+  int RT, KT;                  // row tiles, k tiles
+  int d_in;
+  int batch;                   // 1..8
+  const __half* x;             // R x, [batch][d_in] fp16
+  // output routing (fused groups): member i owns row tiles [rt_begin[i], rt_begin[i+1])
+  int n_out;
+  int rt_begin[kMaxGroup + 1];
+  void* y[kMaxGroup];
+  int ldy[kMaxGroup];          // leading dimension (elements) of y[i] rows (= d_out_i)
+  int y_f32;                   // 1: fp32 output, 0: fp16 output
+  int y_atomic;                // 1: y was zeroed; CTAs sharing a row tile red.add their scaled partials
+  // cross-CTA fixup workspace
+  float* ws;                   // [grid][256] cross-CTA partials (slot = contributing CTA)
+  int* counters;               // [RT], zero between launches (self-resetting)
+  // dequant-only mode
+  __half* w_out;               // [RT*32][d_in] (unscaled W_hat)
+  unsigned long long* timeline; // debug: per-CTA globaltimer stamps [grid][4] (nullptr = off)
+};
+
+struct RhtParams {
+  const void* x;
+  int x_dtype;                 // 0 f16, 1 bf16, 2 f32
+  int batch, d_in, block;
+  const uint32_t* signs;       // d_in bits, 1 = negative
+  __half* out;
+  float scale;                 // 1/sqrt(block)
+  // optional: zero these fp32 outputs (the following GEMV accumulates into them)
+  int n_zero;
+  float* zero_ptr[kMaxGroup];
+  long long zero_n[kMaxGroup];
+};
+
+using GemvLauncher = cudaError_t (*)(const GemvParams&, int grid, int nwarps, bool dequant, bool pdl,
+                                     cudaStream_t s);
+
+// Registry of compiled variants (filled by the instantiation units).
+GemvLauncher find_gemv(const KernelKey& k);
+void register_gemv(const KernelKey& k, GemvLauncher f);
+int gemv_smem_bytes(int nwarps);
+
+cudaError_t launch_rht(const RhtParams& p, bool pdl, cudaStream_t s);
+cudaError_t launch_zero(const RhtParams& p, bool pdl, cudaStream_t s);   // only the n_zero/zero_* fields
+cudaError_t launch_gather_permute(const void* src, void* dst, int world, int batch, int m, int elem_bytes,
+                                  cudaStream_t s);
+void count_launch();
+
+}  // namespace qp

@@ -1,0 +1,220 @@
+// Randomized Hadamard rotation of the activations, x' = (1/sqrt(b)) blockdiag(H_b) D x
+// (P:345-349), plus small utility kernels and the variant registry.
+//
+// One CTA per (block of b inputs, batch row). Each thread holds E consecutive elements:
+// log2(E) butterfly stages in registers, up to 5 stages across lanes with shfl.xor, the
+// remaining stages through shared memory. fp32 arithmetic, one RNE rounding to fp16.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <mutex>
+#include <vector>
+
+#include "qp_internal.h"
+
+namespace qp {
+
+// Zero the fp32 outputs the next GEMV accumulates into (grid-stride over all CTAs).
+__device__ __forceinline__ void zero_outputs(const RhtParams& p) {
+  const long long nthr = (long long)gridDim.x * gridDim.y * blockDim.x;
+  const long long me = ((long long)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int i = 0; i < p.n_zero; ++i) {
+    float4* z = reinterpret_cast<float4*>(p.zero_ptr[i]);
+    const long long n4 = p.zero_n[i] / 4;
+    for (long long j = me; j < n4; j += nthr) z[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (long long j = n4 * 4 + me; j < p.zero_n[i]; j += nthr) p.zero_ptr[i][j] = 0.f;
+  }
+}
+
+__global__ void qp_zero_kernel(const __grid_constant__ RhtParams p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  zero_outputs(p);
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
+template <int E>
+__global__ void __launch_bounds__(1024) qp_rht_kernel(const __grid_constant__ RhtParams p) {
+  extern __shared__ float sx[];
+  const int blk = blockIdx.x, beta = blockIdx.y;
+  const int nthr = p.block / E;
+  const int t = threadIdx.x;
+  const int base = blk * p.block + t * E;     // global input index of v[0]
+  float v[E];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  zero_outputs(p);
+  const size_t row = (size_t)beta * p.d_in;
+  if (p.x_dtype == 0) {
+    const __half* x = reinterpret_cast<const __half*>(p.x) + row + base;
+#pragma unroll
+    for (int i = 0; i < E; i += 8) {
+      const uint4 u = *reinterpret_cast<const uint4*>(x + i);
+      const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __half22float2(h[k]);
+        v[i + 2 * k] = f.x;
+        v[i + 2 * k + 1] = f.y;
+      }
+    }
+  } else if (p.x_dtype == 1) {
+    const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(p.x) + row + base;
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = __bfloat162float(x[i]);
+  } else {
+    const float* x = reinterpret_cast<const float*>(p.x) + row + base;
+#pragma unroll
+    for (int i = 0; i < E; i += 4) {
+      const float4 f = *reinterpret_cast<const float4*>(x + i);
+      v[i] = f.x; v[i + 1] = f.y; v[i + 2] = f.z; v[i + 3] = f.w;
+    }
+  }
+  // D: sign bits (1 = negative), E <= 32 consecutive bits starting at `base`
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const int idx = base + i;
+    if ((__ldg(p.signs + (idx >> 5)) >> (idx & 31)) & 1u) v[i] = -v[i];
+  }
+  // stages inside the thread: strides 1 .. E/2
+#pragma unroll
+  for (int h = 1; h < E; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      if ((i & h) == 0) {
+        const float a = v[i], b = v[i + h];
+        v[i] = a + b;
+        v[i + h] = a - b;
+      }
+    }
+  }
+  // stages across lanes: stride E*m, m = 1..16 (partner thread t ^ m)
+  const int lane = t & 31;
+  for (int m = 1; m < 32 && m < nthr; m <<= 1) {
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const float o = __shfl_xor_sync(0xffffffffu, v[i], m);
+      v[i] = upper ? (o - v[i]) : (v[i] + o);
+    }
+  }
+  // stages across warps through shared memory: strides 32E .. block/2
+  for (int h = 32 * E; h < p.block; h <<= 1) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < E; ++i) sx[t * E + i] = v[i];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int k = t * E + i;
+      const float o = sx[k ^ h];
+      v[i] = (k & h) ? (o - v[i]) : (v[i] + o);
+    }
+  }
+  asm volatile("griddepcontrol.launch_dependents;");
+  __half* out = p.out + row + base;
+#pragma unroll
+  for (int i = 0; i < E; i += 8) {
+    uint4 u;
+    __half2* h = reinterpret_cast<__half2*>(&u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __floats2half2_rn(v[i + 2 * k] * p.scale, v[i + 2 * k + 1] * p.scale);
+    *reinterpret_cast<uint4*>(out + i) = u;
+  }
+  (void)nthr;
+}
+
+cudaError_t launch_rht(const RhtParams& p, bool pdl, cudaStream_t s) {
+  int E = 8;
+  while (p.block / E > 1024) E *= 2;
+  if (E > 32 || p.block / E < 32) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.d_in / p.block, p.batch);
+  cfg.blockDim = dim3(p.block / E);
+  cfg.dynamicSmemBytes = p.block > 32 * E ? p.block * sizeof(float) : 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (E == 8) {
+    e = cudaFuncSetAttribute(qp_rht_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+    if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, qp_rht_kernel<8>, p);
+  } else if (E == 16) {
+    e = cudaFuncSetAttribute(qp_rht_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+    if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, qp_rht_kernel<16>, p);
+  } else {
+    e = cudaFuncSetAttribute(qp_rht_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+    if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, qp_rht_kernel<32>, p);
+  }
+  if (e == cudaSuccess) count_launch();
+  return e;
+}
+
+cudaError_t launch_zero(const RhtParams& p, bool pdl, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(64);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, qp_zero_kernel, p);
+  if (e == cudaSuccess) count_launch();
+  return e;
+}
+
+// [world][batch][m] (all-gather output) -> [batch][world*m]
+__global__ void qp_gather_permute_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int world,
+                                         int batch, int m, int eb) {
+  const long long n = (long long)world * batch * m;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / ((long long)batch * m);
+    const long long rem = i - r * batch * m;
+    const long long b = rem / m, j = rem - b * m;
+    const long long o = b * (long long)world * m + r * m + j;
+    for (int k = 0; k < eb; ++k) dst[o * eb + k] = src[i * eb + k];
+  }
+}
+
+cudaError_t launch_gather_permute(const void* src, void* dst, int world, int batch, int m, int eb, cudaStream_t s) {
+  const long long n = (long long)world * batch * m;
+  int grid = (int)((n + 255) / 256);
+  if (grid > 4096) grid = 4096;
+  qp_gather_permute_kernel<<<grid, 256, 0, s>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), world,
+                                                 batch, m, eb);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---- variant registry ----------------------------------------------------------------
+namespace {
+struct Entry {
+  KernelKey k;
+  GemvLauncher f;
+};
+std::vector<Entry>& registry() {
+  static std::vector<Entry> r;
+  return r;
+}
+std::mutex& registry_mu() {
+  static std::mutex m;
+  return m;
+}
+}  // namespace
+
+void register_gemv(const KernelKey& k, GemvLauncher f) {
+  std::lock_guard<std::mutex> g(registry_mu());
+  registry().push_back({k, f});
+}
+
+GemvLauncher find_gemv(const KernelKey& k) {
+  std::lock_guard<std::mutex> g(registry_mu());
+  for (const auto& e : registry())
+    if (e.k == k) return e.f;
+  return nullptr;
+}
+
+}  // namespace qp

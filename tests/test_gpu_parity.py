@@ -1,0 +1,305 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on the same
+seeded inputs.
+
+Bars:
+  * decoded weights W_hat (qp_dequantize): bit-exact fp16 for every palette quantizer;
+  * y = diag(s) W_hat R x (qp_linear_fwd): per batch row max|y - y*| / max|y*| <= 2e-3
+    (north star; fp16 operands, fp32 accumulation vs fp64; reading R16);
+  * R x (qp_rht_apply): within one fp16 rounding of the fp64 value.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import decode, layout, linear, rht  # noqa: E402
+from qp_synth import activations_fp16, channel_scales, random_code_bytes  # noqa: E402
+
+from . import qp_cases as Q  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+SEED = 7
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_20214_b200 import _lib as L
+    return L
+
+
+_CB = {}
+
+
+def _pair(scheme, bits_x4, L=16):
+    """(library Codebook, oracle codebook dict) from the same frozen fp16 bytes."""
+    Lb = _need_gpu()
+    if not Q.have_codebook(scheme, bits_x4):
+        pytest.skip(f"codebook {Q.codebook_file(scheme, bits_x4)} not built")
+    key = (scheme, bits_x4, L)
+    if key not in _CB:
+        _CB[key] = (Lb.Codebook(scheme, bits_x4, Q.load_fp16(scheme, bits_x4), L=L),
+                    Q.oracle_codebook(scheme, bits_x4, L=L))
+    return _CB[key]
+
+
+_RHT = {}
+
+
+def _rht(d_in):
+    from paper_2509_20214_b200 import _lib as Lb
+    if d_in not in _RHT:
+        _RHT[d_in] = Lb.Rht(SEED, d_in)
+    return _RHT[d_in]
+
+
+def _layer(scheme, bits_x4, d_out, d_in, L=16, layer_id=0):
+    from paper_2509_20214_b200 import _lib as Lb
+    cb, ocb = _pair(scheme, bits_x4, L)
+    r = _rht(d_in)
+    codes = random_code_bytes(Q.code_bytes(d_out, d_in, scheme, bits_x4), layer_id)
+    s = channel_scales(d_out, d_in)
+    lay = Lb.Layer.from_codes(codes, s, d_out, d_in, scheme, bits_x4, cb, r)
+    return lay, codes, s, ocb
+
+
+def _dequant_gpu(lay):
+    W = torch.empty(lay.d_out, lay.d_in, dtype=torch.float16, device="cuda")
+    lay.dequantize(W)
+    torch.cuda.synchronize()
+    return W.cpu().numpy()
+
+
+@pytest.mark.parametrize("scheme,bits_x4", Q.PALETTE)
+def test_dequant_bit_exact_every_quantizer(scheme, bits_x4):
+    # 3 row tiles x 4 k tiles: several tiles, warps and CTAs per launch
+    d_out, d_in = 96, 1024
+    lay, codes, _, ocb = _layer(scheme, bits_x4, d_out, d_in)
+    Wg = _dequant_gpu(lay)
+    Wo = decode.decode_layer(codes, d_out, d_in, scheme, bits_x4, ocb).astype(np.float16)
+    assert np.array_equal(Wg.view(np.uint16), Wo.view(np.uint16))
+
+
+@pytest.mark.parametrize("scheme,bits_x4", [("tcq", 10), ("half_tcq", 13), ("vq", 12), ("nuq", 16)])
+def test_dequant_bit_exact_llama_shape(scheme, bits_x4):
+    d_out, d_in = 4096, 4096
+    lay, codes, _, ocb = _layer(scheme, bits_x4, d_out, d_in, layer_id=3)
+    Wg = _dequant_gpu(lay)
+    Wo = decode.decode_layer(codes, d_out, d_in, scheme, bits_x4, ocb).astype(np.float16)
+    assert np.array_equal(Wg.view(np.uint16), Wo.view(np.uint16))
+
+
+def _fwd(lay, x_np, batch, y_dtype=torch.float32, x_dtype=torch.float16, flags=0):
+    x = torch.from_numpy(np.ascontiguousarray(x_np)).to("cuda", x_dtype)
+    y = torch.empty(batch, lay.d_out, dtype=y_dtype, device="cuda")
+    lay.forward(x, batch, y, flags=flags)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("scheme,bits_x4", Q.TARGET)
+@pytest.mark.parametrize("batch", [1, 3, 8])
+def test_linear_parity_palette(scheme, bits_x4, batch):
+    # ragged: 5 row tiles x 6 k tiles (30 tiles over the persistent grid)
+    d_out, d_in = 160, 1536
+    lay, codes, s, ocb = _layer(scheme, bits_x4, d_out, d_in, layer_id=1)
+    x = activations_fp16(batch, d_in)
+    y = _fwd(lay, x, batch)
+    y_ref = linear.linear_from_codes(codes, d_out, d_in, scheme, bits_x4, ocb, s, x.astype(np.float64), SEED)
+    assert np.max(linear.normwise_error(y, y_ref)) <= TOL
+
+
+@pytest.mark.parametrize("d_out,d_in,scheme,bits_x4", [
+    (4096, 4096, "tcq", 10), (4096, 4096, "half_tcq", 13), (4096, 4096, "tcq", 16),
+    (1024, 14336, "tcq", 10), (512, 28672, "vq", 12), (2048, 8192, "nuq", 16),
+])
+@pytest.mark.parametrize("batch", [1, 8])
+def test_linear_parity_llama_shapes(d_out, d_in, scheme, bits_x4, batch):
+    lay, codes, s, ocb = _layer(scheme, bits_x4, d_out, d_in, layer_id=2)
+    x = activations_fp16(batch, d_in)
+    y = _fwd(lay, x, batch)
+    y_ref = linear.linear_from_codes(codes, d_out, d_in, scheme, bits_x4, ocb, s, x.astype(np.float64), SEED)
+    assert np.max(linear.normwise_error(y, y_ref)) <= TOL
+
+
+@pytest.mark.parametrize("d_out,d_in,bits_x4", [(14336, 4096, 10), (4096, 14336, 13), (28672, 8192, 16)])
+def test_full_size_sampled_rows(d_out, d_in, bits_x4):
+    """BASELINE shapes at full size: GPU y against the oracle on sampled row tiles."""
+    scheme = "half_tcq" if bits_x4 % 2 else "tcq"
+    lay, codes, s, ocb = _layer(scheme, bits_x4, d_out, d_in, layer_id=5)
+    batch = 2
+    x = activations_fp16(batch, d_in)
+    y = _fwd(lay, x, batch)
+    offs, _ = layout.tile_offsets(d_out, d_in, scheme, bits_x4)
+    rowtile_bytes = offs[1, 0] if offs.shape[0] > 1 else len(codes)
+    xr = rht.rht_apply(x.astype(np.float64), SEED)
+    for rt in (0, 1, d_out // 32 // 2, d_out // 32 - 1):
+        sub = codes[rt * rowtile_bytes:(rt + 1) * rowtile_bytes]
+        W = decode.decode_layer(sub, 32, d_in, scheme, bits_x4, ocb)
+        y_ref = (xr @ W.T) * s[rt * 32:(rt + 1) * 32][None, :]
+        err = np.max(np.abs(y[:, rt * 32:(rt + 1) * 32] - y_ref)) / np.max(np.abs(y_ref))
+        assert err <= 4 * TOL      # normalised by this 32-row slice's max (a stricter base)
+
+
+def test_rht_kernel_vs_oracle():
+    Lb = _need_gpu()
+    for d_in in (256, 4096, 14336, 28672, 8192):
+        r = Lb.Rht(SEED, d_in)
+        x = activations_fp16(3, d_in)
+        xg = torch.from_numpy(x).cuda()
+        out = torch.empty(3, d_in, dtype=torch.float16, device="cuda")
+        r.apply(xg, 3, out)
+        torch.cuda.synchronize()
+        ref = rht.rht_apply(x.astype(np.float64), SEED)
+        got = out.float().cpu().numpy()
+        # within one fp16 rounding (relative 2^-11) plus fp32 summation noise
+        assert np.all(np.abs(got - ref) <= np.abs(ref) * 2 ** -10 + 1e-6 * np.abs(x).max())
+
+
+def test_input_dtypes_and_prerotated():
+    Lb = _need_gpu()
+    lay, codes, s, ocb = _layer("tcq", 10, 96, 768)
+    x = activations_fp16(2, 768)
+    y_ref = linear.linear_from_codes(codes, 96, 768, "tcq", 10, ocb, s, x.astype(np.float64), SEED)
+    for xd in (torch.float16, torch.bfloat16, torch.float32):
+        y = _fwd(lay, x, 2, x_dtype=xd)
+        assert np.max(linear.normwise_error(y, y_ref)) <= TOL
+    y16 = _fwd(lay, x, 2, y_dtype=torch.float16)
+    assert np.max(linear.normwise_error(y16, y_ref)) <= TOL
+    # QP_X_PREROTATED: feed R x from qp_rht_apply
+    r = Lb.Rht(SEED, 768)
+    xr = torch.empty(2, 768, dtype=torch.float16, device="cuda")
+    r.apply(torch.from_numpy(x).cuda(), 2, xr)
+    y2 = torch.empty(2, 96, dtype=torch.float32, device="cuda")
+    lay.forward(xr, 2, y2, flags=Lb.QP_X_PREROTATED)
+    torch.cuda.synchronize()
+    assert np.max(linear.normwise_error(y2.cpu().numpy(), y_ref)) <= TOL
+
+
+def test_edge_cases_and_errors():
+    Lb = _need_gpu()
+    # smallest layer: a single tile (32 x 256), batch at the maximum 8
+    lay, codes, s, ocb = _layer("vq", 8, 32, 256)
+    x = activations_fp16(8, 256)
+    y = _fwd(lay, x, 8)
+    y_ref = linear.linear_from_codes(codes, 32, 256, "vq", 8, ocb, s, x.astype(np.float64), SEED)
+    assert np.max(linear.normwise_error(y, y_ref)) <= TOL
+    # repeated launches reuse the self-resetting fixup counters
+    for _ in range(3):
+        assert np.array_equal(_fwd(lay, x, 8), y)
+    xg = torch.from_numpy(x).cuda()
+    yg = torch.empty(9, 32, device="cuda")
+    for bad in (0, 9):
+        with pytest.raises(Lb.QPError) as e:
+            lay.forward(xg, bad, yg)
+        assert e.value.status == 3
+    cb, _ = _pair("vq", 8)
+    with pytest.raises(Lb.QPError) as e:
+        Lb.Layer.from_codes(np.zeros(10, np.uint8), np.ones(40, np.float32), 40, 256, "vq", 8, cb, Lb.Rht(1, 256))
+    assert e.value.status == 3
+    with pytest.raises(Lb.QPError) as e:
+        Lb.Layer.from_codes(np.zeros(10, np.uint8), np.ones(32, np.float32), 32, 256, "vq", 8, cb, Lb.Rht(1, 256))
+    assert e.value.status == 6
+
+
+def test_deterministic_and_atomic_paths():
+    """fp32 y defaults to zero-then-add across CTAs; QP_DETERMINISTIC (and fp16 y) use the
+    in-order reduction, which is bitwise reproducible. Both meet the parity bar."""
+    Lb = _need_gpu()
+    lay, codes, s, ocb = _layer("tcq", 10, 4096, 4096)
+    x = activations_fp16(4, 4096)
+    y_ref = linear.linear_from_codes(codes, 4096, 4096, "tcq", 10, ocb, s, x.astype(np.float64), SEED)
+    y1 = _fwd(lay, x, 4, flags=Lb.QP_DETERMINISTIC)
+    y2 = _fwd(lay, x, 4, flags=Lb.QP_DETERMINISTIC)
+    assert np.array_equal(y1, y2)
+    ya = _fwd(lay, x, 4)
+    for y in (y1, ya):
+        assert np.max(linear.normwise_error(y, y_ref)) <= TOL
+    assert np.max(np.abs(ya - y1)) <= 1e-5 * np.max(np.abs(y1))
+
+
+def test_fused_group_qkv_and_upgate():
+    Lb = _need_gpu()
+    for shapes, scheme, bits in ([(128, 512), (64, 512), (64, 512)], "half_tcq", 17),   \
+                                ([(448, 1024), (448, 1024)], "tcq", 12):
+        layers, refs = [], []
+        x = activations_fp16(3, shapes[0][1])
+        for i, (do, di) in enumerate(shapes):
+            lay, codes, s, ocb = _layer(scheme, bits, do, di, layer_id=10 + i)
+            layers.append(lay)
+            refs.append(linear.linear_from_codes(codes, do, di, scheme, bits, ocb, s, x.astype(np.float64), SEED))
+        g = Lb.Group(layers)
+        xg = torch.from_numpy(x).cuda()
+        ys = [torch.empty(3, do, device="cuda") for do, _ in shapes]
+        g.forward(xg, 3, ys)
+        torch.cuda.synchronize()
+        for y, ref in zip(ys, refs):
+            assert np.max(linear.normwise_error(y.cpu().numpy(), ref)) <= TOL
+
+
+def test_row_shards_concatenate():
+    lay, codes, s, ocb = _layer("tcq", 8, 256, 1024)
+    x = activations_fp16(2, 1024)
+    y_full = _fwd(lay, x, 2)
+    parts = []
+    for rank in range(4):
+        sh = lay.shard(rank, 4)
+        parts.append(_fwd(sh, x, 2))
+    y_cat = np.concatenate(parts, axis=1)
+    y_ref = linear.linear_from_codes(codes, 256, 1024, "tcq", 8, ocb, s, x.astype(np.float64), SEED)
+    assert np.max(linear.normwise_error(y_cat, y_ref)) <= TOL
+    assert np.max(np.abs(y_cat - y_full)) <= 1e-5 * np.max(np.abs(y_full))
+
+
+def test_sharded_forward_nccl_world1():
+    Lb = _need_gpu()
+    lay, codes, s, ocb = _layer("vq", 12, 256, 512)
+    comm = Lb.NcclComm(Lb.NcclComm.unique_id(), 1, 0)
+    try:
+        for batch in (1, 4):
+            x = activations_fp16(batch, 512)
+            xg = torch.from_numpy(x).cuda()
+            y = torch.empty(batch, 256, device="cuda")
+            lay.shard(0, 1).forward_sharded(xg, batch, y, comm)
+            torch.cuda.synchronize()
+            y_ref = linear.linear_from_codes(codes, 256, 512, "vq", 12, ocb, s, x.astype(np.float64), SEED)
+            assert np.max(linear.normwise_error(y.cpu().numpy(), y_ref)) <= TOL
+    finally:
+        comm.close()
+
+
+def test_offline_quantizer_c1_matches_oracle():
+    """Config C1: 256x256 TCQ-2.0, L=12 (reading R1), W ~ N(0,1) seed 0. The C++ encoder and
+    the oracle's rotate-half Viterbi agree by path cost (reading R5); decoding is bit-exact."""
+    Lb = _need_gpu()
+    from qp_synth import gaussian_weights
+    cb, ocb = _pair("tcq", 8, L=12)
+    W = gaussian_weights(256, 256, seed=0)
+    lay = Lb.Layer.quantize_offline(W.astype(np.float32), "tcq", 8, cb, Lb.Rht(SEED, 256))
+    codes_g, s_g = lay.codes(), lay.scales()
+    codes_o, s_o = linear.quantize_offline(W.astype(np.float32).astype(np.float64), "tcq", 8, ocb, SEED)
+    assert np.allclose(s_g, s_o, rtol=1e-6)
+    Wt, _ = linear.gaussianize(W.astype(np.float32).astype(np.float64), SEED)
+    Wg = decode.decode_layer(codes_g, 256, 256, "tcq", 8, ocb)
+    Wo = decode.decode_layer(codes_o, 256, 256, "tcq", 8, ocb)
+    dg, do = np.sum((Wg - Wt) ** 2), np.sum((Wo - Wt) ** 2)
+    assert abs(dg - do) / do < 1e-6
+    assert np.mean(codes_g == codes_o) > 0.99
+    assert np.array_equal(_dequant_gpu(lay).view(np.uint16), Wg.astype(np.float16).view(np.uint16))
+    x = activations_fp16(1, 256)
+    y = _fwd(lay, x, 1)
+    y_ref = linear.linear_ref(Wg, s_g.astype(np.float64), x.astype(np.float64), SEED)
+    assert np.max(linear.normwise_error(y, y_ref)) <= TOL
+
+
+@pytest.mark.parametrize("scheme,bits_x4", [("nuq", 12), ("vq", 10), ("unif", 16)])
+def test_offline_rtn_matches_oracle(scheme, bits_x4):
+    Lb = _need_gpu()
+    from qp_synth import gaussian_weights
+    cb, ocb = _pair(scheme, bits_x4)
+    W = gaussian_weights(64, 512, seed=4).astype(np.float32)
+    lay = Lb.Layer.quantize_offline(W, scheme, bits_x4, cb, Lb.Rht(SEED, 512))
+    codes_o, s_o = linear.quantize_offline(W.astype(np.float64), scheme, bits_x4, ocb, SEED)
+    assert np.allclose(lay.scales(), s_o, rtol=1e-6)
+    assert np.mean(lay.codes() == codes_o) > 0.99
