@@ -119,12 +119,29 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void load_x8(uint32_t* dst, const __half* src) {   // 8 regs = 16 halves
+  const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(src));
+  const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+  dst[0] = v0.x; dst[1] = v0.y; dst[2] = v0.z; dst[3] = v0.w;
+  dst[4] = v1.x; dst[5] = v1.y; dst[6] = v1.z; dst[7] = v1.w;
+}
+
 // Decode one tile's 128 steps of this lane and multiply-accumulate (GEMV) or store (dequant).
+// x' B fragments: xb[0..15] (kappa 0..7) and xb[16..31] (kappa 8..15). The second half of this
+// tile's activations (x_hi) is loaded when the tile starts and the first half of the next tile's
+// (x_next) once kappa 0..7 are done, so activation loads never sit on the critical path and
+// need no extra registers. Lanes with no batch row (x_hi == nullptr) keep zeros.
 template <int MODE, int C, int L, int TB, int REPS, bool DEQ>
-__device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff,
-                                          const uint32_t* xb, float (&acc)[2][4], uint32_t* wout_lane,
-                                          int ldw_words) {
+__device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, uint32_t* xb, float (&acc)[2][4],
+                                          uint32_t* wout_lane, int ldw_words, const __half* x_hi,
+                                          const __half* x_next) {
   using D = Dec<MODE, C, L, TB, REPS>;
+  if constexpr (!DEQ) {
+    if (x_hi) {
+      load_x8(xb + 16, x_hi);
+      load_x8(xb + 24, x_hi + 16);
+    }
+  }
   static_for<16>([&](auto KAP) {
     constexpr int kap = decltype(KAP)::value;
     static_for<2>([&](auto M) {
@@ -145,17 +162,25 @@ __device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff,
         mma16816(acc[m], a0, a1, a2, a3, xb[2 * kap], xb[2 * kap + 1]);
       }
     });
+    if constexpr (!DEQ && kap == 7) {
+      if (x_next) {
+        load_x8(xb, x_next);
+        load_x8(xb + 8, x_next + 16);
+      }
+    }
   });
 }
 
-template <int MODE, int REPS>
-__device__ __forceinline__ void build_table(const uint32_t* __restrict__ g, int words, uint8_t* tab, uint32_t* stage) {
-  // 1. compact table (<= 8 KB) -> shared staging area with 128-bit loads (one round trip)
+// 1. compact table (<= 16 KB) -> shared staging area with 128-bit loads (one round trip)
+__device__ __forceinline__ void stage_table(const uint32_t* __restrict__ g, int words, uint32_t* stage) {
   for (int i = threadIdx.x * 4; i < words; i += blockDim.x * 4)
     *reinterpret_cast<uint4*>(stage + i) = __ldg(reinterpret_cast<const uint4*>(g + i));
-  __syncthreads();
-  // 2. expand: entry e, replica r at byte e*REPS*4 + r*4 (bank = replica = lane mod REPS).
-  //    A warp writes 512 contiguous bytes per STS.128 instruction (conflict-free).
+}
+
+// 2. expand: entry e, replica r at byte e*REPS*4 + r*4 (bank = replica = lane mod REPS).
+//    A warp writes 512 contiguous bytes per STS.128 instruction (conflict-free).
+template <int REPS>
+__device__ __forceinline__ void expand_table(int words, uint8_t* tab, const uint32_t* stage) {
   constexpr int V4 = REPS / 4;
   const int total = words * V4;
 #pragma unroll 4
@@ -210,6 +235,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
   const int KH = p.KT / 2;
   const long long rowtile_bytes = (long long)KH * 512 * CLO + (long long)(KT - KH) * 512 * CHI;
 
+  uint64_t pol_keep, pol_stream;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
   auto tile_ptr = [&](uint32_t rt, int kt) -> const uint8_t* {
     const long long off = (long long)rt * rowtile_bytes + (kt < KH ? (long long)kt * 512 * CLO
                                                         : (long long)KH * 512 * CLO + (long long)(kt - KH) * 512 * CHI);
@@ -222,18 +250,31 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
     for (int i = 0; i < CMAX; ++i) {
       if (CLO == CHI || i < c) {
         uint4 v;
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + i * 32));
+        // streamed exactly once: no L1 allocation, first out of L2
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + i * 32), "l"(pol_stream));
         buf[4 * i] = v.x; buf[4 * i + 1] = v.y; buf[4 * i + 2] = v.z; buf[4 * i + 3] = v.w;
       }
     }
   };
 
+  // The compact decode table is on the critical path of the prologue: request it before the
+  // first code tiles flood the memory queues, and keep it resident in L2 across launches.
+  constexpr int kStageV4 = 4;   // <= 4 x 16 B per thread: tables up to 32 KB with 512 threads
+  uint4 tstage[kStageV4];
+#pragma unroll
+  for (int k = 0; k < kStageV4; ++k) {
+    const int i = (threadIdx.x + k * NWARP * 32) * 4;
+    if (i < p.table_words)
+      asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=r"(tstage[k].x), "=r"(tstage[k].y), "=r"(tstage[k].z), "=r"(tstage[k].w)
+                   : "l"(p.table + i), "l"(pol_keep));
+  }
+
   uint32_t cur[4 * CMAX], nxt[4 * CMAX];
   uint32_t rt = a / KT;
   int kt = (int)(a - rt * KT);
   const uint8_t* ptr = tile_ptr(rt, kt);
-  if (a < b) load_tile(ptr, kt, cur);      // codes are immutable: safe before the PDL wait
 
   // per-row scales of this CTA's row tiles -> registers now, shared memory after the table build
   float* sscale = reinterpret_cast<float*>(smem + kSmemTableBytes + NWARP * 2 * 256 * 4);
@@ -247,29 +288,37 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
     const int i = tid + k * NWARP * 32;
     sc_reg[k] = (!DEQ && scales_in_smem && i < n_srt * kTileRows) ? __ldg(p.scales + srt0 * kTileRows + i) : 0.f;
   }
-  // activations of the first tile: produced by the previous kernel, so only after the PDL wait;
-  // their L2 latency overlaps the table build below
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   uint32_t xb[32];
-  auto load_x = [&](int kt_) {
-    if (g < p.batch) {
-      const uint4* xs = reinterpret_cast<const uint4*>(p.x + (size_t)g * p.d_in + kt_ * kTileCols + 64 * q);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint4 v = __ldg(xs + i);
-        xb[4 * i] = v.x; xb[4 * i + 1] = v.y; xb[4 * i + 2] = v.z; xb[4 * i + 3] = v.w;
-      }
-    } else {
+  for (int i = 0; i < 32; ++i) xb[i] = 0u;
+  const bool xrow = !DEQ && g < p.batch;           // this lane holds a batch row of x'
+  const __half* xlane = p.x + (size_t)g * p.d_in + 64 * q;
+  // Everything above and the table build read only immutable layer data, so under programmatic
+  // dependent launch they overlap the previous kernel (the activation rotation). x' and y are
+  // touched only after the wait.
 #pragma unroll
-      for (int i = 0; i < 32; ++i) xb[i] = 0u;
-    }
-  };
-  if (!DEQ && a < b) load_x(kt);
-  build_table<MODE, REPS>(p.table, p.table_words, tab, reinterpret_cast<uint32_t*>(part));
+  for (int k = 0; k < kStageV4; ++k) {
+    const int i = (threadIdx.x + k * NWARP * 32) * 4;
+    if (i < p.table_words) *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(part) + i) = tstage[k];
+  }
+  __syncthreads();
+  stamp(7);
+  // first tile's codes: issued once the table has arrived (so the table request did not queue
+  // behind ~10 MB of code requests), they land while the table is expanded. Codes are immutable:
+  // safe before the PDL wait.
+  if (a < b) load_tile(ptr, kt, cur);
+  expand_table<REPS>(p.table_words, tab, reinterpret_cast<const uint32_t*>(part));
+  stamp(6);
 #pragma unroll
   for (int k = 0; k < SC_PER_THREAD; ++k) {
     const int i = tid + k * NWARP * 32;
     if (!DEQ && scales_in_smem && i < n_srt * kTileRows) sscale[i] = sc_reg[k];
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stamp(5);
+  if (xrow && a < b) {                             // first tile, kappa 0..7
+    load_x8(xb, xlane + kt * kTileCols);
+    load_x8(xb + 8, xlane + kt * kTileCols + 16);
   }
   __syncthreads();
   auto scale_of = [&](uint32_t rt_, int row) -> float {
@@ -281,18 +330,16 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
   float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
   const uint32_t a_rt = a / KT;
 
-  for (uint32_t t = a; t < b; ++t) {
+  // One tile: prefetch the next tile's stream into `nb`, decode `cb`. (Ping-ponging the two
+  // buffers instead of copying doubles the code size and measured no faster on B200.)
+  auto process = [&](uint32_t t, uint32_t (&cb)[4 * CMAX], uint32_t (&nb)[4 * CMAX]) {
     int kt_n = kt + 1;
     uint32_t rt_n = rt;
-    if (kt_n == KT) { kt_n = 0; ++rt_n; }
+    if (kt_n == (int)KT) { kt_n = 0; ++rt_n; }
     const uint8_t* ptr_n = (CLO == CHI) ? ptr + 512 * CLO : tile_ptr(rt_n, kt_n);
-    if (t + 1 < b) {
-      load_tile(ptr_n, kt_n, nxt);
-      if constexpr (!DEQ) {
-        if (g < p.batch)   // next tile's activations -> L1 (no registers held)
-          asm volatile("prefetch.global.L1 [%0];" :: "l"(p.x + (size_t)g * p.d_in + kt_n * kTileCols + 64 * q));
-      }
-    }
+    if (t + 1 < b) load_tile(ptr_n, kt_n, nb);
+    const __half* x_hi = xrow ? xlane + kt * kTileCols + 32 : nullptr;
+    const __half* x_next = (xrow && t + 1 < b) ? xlane + kt_n * kTileCols : nullptr;
     uint32_t* wout_lane = nullptr;
     int ldw = 0;
     if constexpr (DEQ) {
@@ -300,13 +347,12 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
       wout_lane = reinterpret_cast<uint32_t*>(p.w_out) + (size_t)(rt * kTileRows + g) * ldw + (kt * kTileCols + 64 * q) / 2;
     }
     if (CLO == CHI || kt < KH)
-      tile_body<MODE, CLO, L, TB, REPS, DEQ>(cur, laneoff, xb, acc, wout_lane, ldw);
+      tile_body<MODE, CLO, L, TB, REPS, DEQ>(cb, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next);
     else
-      tile_body<MODE, CHI, L, TB, REPS, DEQ>(cur, laneoff, xb, acc, wout_lane, ldw);
-    if (!DEQ && t + 1 < b) load_x(kt_n);      // L1 hit: prefetched one tile ahead
+      tile_body<MODE, CHI, L, TB, REPS, DEQ>(cb, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next);
 
     if constexpr (!DEQ) {
-      if (kt == KT - 1 || t == b - 1) {
+      if (kt == (int)KT - 1 || t == b - 1) {
         const uint32_t rs = rt * KT;
         const bool own = (a <= rs) && (b >= rs + KT);
         if (own) {
@@ -333,9 +379,12 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
           for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
       }
     }
+    kt = kt_n; rt = rt_n; ptr = ptr_n;
+  };
+  for (uint32_t t = a; t < b; ++t) {
+    process(t, cur, nxt);
 #pragma unroll
     for (int i = 0; i < 4 * CMAX; ++i) cur[i] = nxt[i];
-    kt = kt_n; rt = rt_n; ptr = ptr_n;
   }
   stamp(2);
   asm volatile("griddepcontrol.launch_dependents;");
@@ -370,7 +419,6 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
         for (int k = 0; k < 8; ++k) v[k] += sl[lane + 32 * k];
       }
     }
-    stamp(5);
     if (T0 <= rs && T1 >= re) {                          // the whole row tile is in this CTA
       if (act)
 #pragma unroll
@@ -417,7 +465,6 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
       p.counters[rt] = 0;                                 // every contributor has arrived: reset
     }
     __syncwarp();
-    stamp(6);
     if (act) {
       constexpr int kMaxContrib = 8;
       float pv[kMaxContrib][8];
@@ -442,33 +489,40 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
   stamp(3);
 }
 
-template <int MODE, int CLO, int CHI, int L, int TB, int REPS>
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, int NW>
+cudaError_t launch_nw(const GemvParams& prm, int grid, bool pdl, cudaStream_t s) {
+  const int smem = kSmemTableBytes + NW * 2 * 256 * 4 + kMaxScaleTiles * kTileRows * 4;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, DEQ, NW>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k, prm);
+  return e;
+}
+
+int tune_nwarp();   // QP_NWARP environment override (tuning experiments), 0 = default
+
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool TUNE = false>
 struct GemvVariant {
   static constexpr int CMAX = CLO > CHI ? CLO : CHI;
   static constexpr int NWARP = CMAX <= 6 ? 16 : 12;
   static cudaError_t launch(const GemvParams& prm, int grid, int /*nwarps*/, bool dequant, bool pdl, cudaStream_t s) {
-    const int smem = kSmemTableBytes + NWARP * 2 * 256 * 4 + kMaxScaleTiles * kTileRows * 4;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(NWARP * 32);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e;
-    if (dequant) {
-      auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, true, NWARP>;
-      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k, prm);
-    } else {
-      auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, false, NWARP>;
-      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k, prm);
+    if (dequant) return launch_nw<MODE, CLO, CHI, L, TB, REPS, true, NWARP>(prm, grid, pdl, s);
+    if constexpr (TUNE) {
+      const int nw = tune_nwarp();
+      if (nw == 8) return launch_nw<MODE, CLO, CHI, L, TB, REPS, false, 8>(prm, grid, pdl, s);
+      if (nw == 12) return launch_nw<MODE, CLO, CHI, L, TB, REPS, false, 12>(prm, grid, pdl, s);
+      if (nw == 16 && CMAX <= 8) return launch_nw<MODE, CLO, CHI, L, TB, REPS, false, (CMAX <= 8 ? 16 : 12)>(prm, grid, pdl, s);
     }
-    return e;
+    return launch_nw<MODE, CLO, CHI, L, TB, REPS, false, NWARP>(prm, grid, pdl, s);
   }
   static void reg() { register_gemv(KernelKey{MODE, CLO, CHI, L, TB, REPS}, &launch); }
 };

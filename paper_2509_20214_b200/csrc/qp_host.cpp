@@ -344,8 +344,8 @@ qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, co
       }
     }
     fprintf(stderr, "kcyc (avg/max over CTAs):");
-    const char* nm[8] = {"", "table", "mainend", "epiend", "epistart", "psum", "atomic", ""};
-    for (int k = 1; k < 7; ++k) fprintf(stderr, " %s %.2f/%.2f", nm[k], cnt[k] ? av[k] / cnt[k] : 0.0, mx[k]);
+    const char* nm[8] = {"", "table", "mainend", "epiend", "epistart", "afterwait", "afterexpand", "afterstage"};
+    for (int k = 1; k < 8; ++k) fprintf(stderr, " %s %.2f/%.2f", nm[k], cnt[k] ? av[k] / cnt[k] : 0.0, mx[k]);
     fprintf(stderr, "\n");
     cudaMemset(d_tl, 0, 4096 * 128 * 8);
   }
@@ -592,14 +592,14 @@ qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch
   const bool atomic = yt == QP_F32 && !(flags & QP_DETERMINISTIC);
   const long long zn[1] = {(long long)batch * l->d_out};
   if (!(flags & QP_X_PREROTATED)) {
-    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, false, s, atomic ? 1 : 0, ys, zn)) != QP_OK) return st;
+    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, pdl, s, atomic ? 1 : 0, ys, zn)) != QP_OK) return st;
     xr = l->d_xrot;
   } else if (atomic) {
     RhtParams zp{};
     zp.n_zero = 1;
     zp.zero_ptr[0] = static_cast<float*>(y);
     zp.zero_n[0] = zn[0];
-    cudaError_t e = launch_zero(zp, false, s);
+    cudaError_t e = launch_zero(zp, pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "zero kernel launch");
   }
   const int rtb[2] = {0, l->d_out / kTileRows};
@@ -688,7 +688,7 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
   long long zn[kMaxGroup];
   for (int i = 0; i < n; ++i) zn[i] = (long long)batch * g->d_outs[i];
   if (!(flags & QP_X_PREROTATED)) {
-    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, false, s, atomic ? n : 0, ys, zn)) != QP_OK) return st;
+    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, !(flags & QP_NO_PDL), s, atomic ? n : 0, ys, zn)) != QP_OK) return st;
     xr = l->d_xrot;
   } else if (atomic) {
     RhtParams zp{};
@@ -697,7 +697,7 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
       zp.zero_ptr[i] = static_cast<float*>(ys[i]);
       zp.zero_n[i] = zn[i];
     }
-    cudaError_t e = launch_zero(zp, false, s);
+    cudaError_t e = launch_zero(zp, !(flags & QP_NO_PDL), s);
     if (e != cudaSuccess) return cuda_fail(e, "zero kernel launch");
   }
   int rtb[kMaxGroup + 1];

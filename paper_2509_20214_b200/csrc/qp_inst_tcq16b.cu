@@ -6,7 +6,7 @@ namespace {
 struct Register {
   Register() {
     GemvVariant<DEC_TCQ_PRESIGNED, 7, 7, 16, 9, 32>::reg();
-    GemvVariant<DEC_TCQ_PRESIGNED, 8, 8, 16, 9, 32>::reg();
+    GemvVariant<DEC_TCQ_PRESIGNED, 8, 8, 16, 9, 32, true>::reg();
     GemvVariant<DEC_TCQ_UNSIGNED, 9, 9, 16, 10, 32>::reg();
     GemvVariant<DEC_TCQ_UNSIGNED, 10, 10, 16, 11, 16>::reg();
   }

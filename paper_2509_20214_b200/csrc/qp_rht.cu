@@ -7,6 +7,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -27,9 +28,9 @@ __device__ __forceinline__ void zero_outputs(const RhtParams& p) {
 }
 
 __global__ void qp_zero_kernel(const __grid_constant__ RhtParams p) {
+  asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   zero_outputs(p);
-  asm volatile("griddepcontrol.launch_dependents;");
 }
 
 template <int E>
@@ -40,6 +41,9 @@ __global__ void __launch_bounds__(1024) qp_rht_kernel(const __grid_constant__ Rh
   const int t = threadIdx.x;
   const int base = blk * p.block + t * E;     // global input index of v[0]
   float v[E];
+  // Let the dependent GEMV start its prologue (code prefetch, decode-table build) right away;
+  // it waits for this grid's completion before it reads x' or touches y.
+  asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   zero_outputs(p);
   const size_t row = (size_t)beta * p.d_in;
@@ -109,7 +113,6 @@ __global__ void __launch_bounds__(1024) qp_rht_kernel(const __grid_constant__ Rh
       v[i] = (k & h) ? (o - v[i]) : (v[i] + o);
     }
   }
-  asm volatile("griddepcontrol.launch_dependents;");
   __half* out = p.out + row + base;
 #pragma unroll
   for (int i = 0; i < E; i += 8) {
@@ -187,6 +190,15 @@ cudaError_t launch_gather_permute(const void* src, void* dst, int world, int bat
                                                  batch, m, eb);
   count_launch();
   return cudaGetLastError();
+}
+
+int tune_nwarp() {
+  static int n = -1;
+  if (n < 0) {
+    const char* e = getenv("QP_NWARP");
+    n = e ? atoi(e) : 0;
+  }
+  return n;
 }
 
 // ---- variant registry ----------------------------------------------------------------
