@@ -286,42 +286,46 @@ def main():
     step_bytes = gemv_bytes + rht_bytes
     value = step_bytes / (ms * 1e-3) / 1e9
 
-    # ---- per-kernel timing of the fused GEMV (pre-rotated x, no PDL, events per launch) -----
+    # ---- per-kernel timing of the fused GEMV: one CUDA graph per layer shape/width holding
+    #      back-to-back launches over the replicas (pre-rotated x, fp16 y so no zeroing kernel),
+    #      timed with events on the launching stream -------------------------------------------
     xr = {}
     for inst in insts:
         d_in = inst["meta"]["d_in"]
         if d_in not in xr:
             xr[d_in] = torch.empty(batch, d_in, dtype=torch.float16, device=dev)
             rots[d_in].apply(inst["x"], batch, xr[d_in])
+    y16 = {L["d_out"]: torch.empty(batch, L["m"], dtype=torch.float16, device=dev) for L in layers}
     torch.cuda.synchronize()
-    gemv_ms = []
-    gemv_alg = 0
-    with torch.cuda.stream(stream):
-        evs = []
-        reps_k = max(3, min(args.steps, 10))
-        for it in range(reps_k + 1):
-            for inst in insts:
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                inst["layer"].forward(xr[inst["meta"]["d_in"]], batch, inst["y"],
-                                      flags=QL.QP_X_PREROTATED | QL.QP_NO_PDL, stream=stream)
-                b.record(stream)
-                if it > 0:
-                    evs.append((a, b, inst))
-        stream.synchronize()
-    for a, b, inst in evs:
-        gemv_ms.append(a.elapsed_time(b))
-        L = inst["meta"]
-        gemv_alg += layer_bytes(L["m"], L["d_in"], L["bits_x4"], L["tb"], batch)[0]
-    gemv_avg_ms = statistics.mean(gemv_ms)
-    gemv_achieved = gemv_alg / (sum(gemv_ms) * 1e-3) / 1e9
+    per_layer_us, gemv_time_s, gemv_alg = {}, 0.0, 0
+    n_rep = 8
+    for li, L in enumerate(layers):
+        group = [insts[rep * n_layers + li] for rep in range(REPLICAS)]
+        with torch.cuda.stream(stream):
+            for inst in group:
+                inst["layer"].forward(xr[L["d_in"]], batch, y16[L["d_out"]], flags=QL.QP_X_PREROTATED, stream=stream)
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for k in range(n_rep):
+                    group[k % REPLICAS]["layer"].forward(xr[L["d_in"]], batch, y16[L["d_out"]],
+                                                         flags=QL.QP_X_PREROTATED, stream=stream)
+            for _ in range(3):
+                g.replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(3, min(args.steps, 20))
+            a.record(stream)
+            for _ in range(reps):
+                g.replay()
+            b.record(stream)
+            b.synchronize()
+        us = a.elapsed_time(b) * 1e3 / (reps * n_rep)
+        per_layer_us[f'{L["d_out"]}x{L["d_in"]}@{L["bits_x4"] / 4:g}b'] = round(us, 3)
+        gemv_time_s += us * 1e-6
+        gemv_alg += layer_bytes(L["m"], L["d_in"], L["bits_x4"], L["tb"], batch)[0] - 2 * batch * L["m"]
+    gemv_achieved = gemv_alg / gemv_time_s / 1e9          # fp16 y: 2 bytes per output, not 4
+    gemv_avg_ms = gemv_time_s / n_layers * 1e3
     peak, peak_kind = measured_peaks()
-    per_layer_us = {}
-    for (a, b, inst) in evs:
-        L = inst["meta"]
-        k = f'{L["d_out"]}x{L["d_in"]}@{L["bits_x4"] / 4:g}b'
-        per_layer_us.setdefault(k, []).append(a.elapsed_time(b) * 1e3)
-    per_layer_us = {k: round(statistics.median(v), 2) for k, v in per_layer_us.items()}
 
     # ---- end to end through the public API with host buffers (N=1 only) ------------------
     e2e = None
@@ -372,7 +376,8 @@ def main():
                        "gemv_us_per_layer": per_layer_us},
             "roofline": {"bound": "hbm", "achieved": round(gemv_achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(gemv_achieved / peak, 4), "traffic": None,
-                         "kernel": "qp_gemv_kernel (fused dequant-GEMV), all 9 layers, events per launch",
+                         "kernel": "qp_gemv_kernel (fused dequant-GEMV), all 9 layers, CUDA graph of back-to-back "
+                                   "launches per layer, events on the launching stream",
                          "peak_kind": peak_kind, "avg_launch_us": round(gemv_avg_ms * 1e3, 3)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches_per_step * args.steps),
             "clocks": ck,

@@ -60,7 +60,7 @@ struct Viterbi {
   std::vector<double> D, Dn;
   std::vector<uint16_t> bp;         // [n][2^(L-s)]
   Viterbi(int L_, int s_, int n_, const std::vector<double>* lut_) : L(L_), s(s_), n(n_), lut(lut_) {
-    const int ns = 1 << (L - s);
+    const int ns = 1 << (L >= s ? L - s : 0);
     D.resize(ns);
     Dn.resize(ns);
     bp.resize((size_t)n * ns);
@@ -226,7 +226,8 @@ qp_status qp_quantize_offline(const float* W_host, int d_out, int d_in, qp_schem
   auto worker = [&]() {
     std::vector<double> v(256);
     std::vector<uint32_t> win(128);
-    Viterbi vlo(L, c_lo, 128, &lut), vhi(L, c_hi, 128, &lut);
+    // trellis state only for TCQ (L = 0 for the other schemes)
+    Viterbi vlo(tcq ? L : c_lo, c_lo, 128, &lut), vhi(tcq ? L : c_hi, c_hi, 128, &lut);
     for (;;) {
       const long long u = next.fetch_add(1);
       if (u >= units) break;
