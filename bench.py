@@ -235,20 +235,37 @@ def main():
             inst["layer"].forward(inst["x"], batch, inst["y"], flags=flags, stream=stream)
 
     # ---- capture one graph per replica ------------------------------------------------
+    # (QP_BENCH_EAGER=1 replays the step eagerly instead: ncu cannot profile our kernels inside
+    #  captured graphs, so the launch-list profile in profiles/ is taken that way.)
     stream = torch.cuda.Stream(device=dev)
     n_layers = len(layers)
     graphs = []
+    eager = os.environ.get("QP_BENCH_EAGER") == "1"
+
+    class EagerStep:
+        def __init__(self, rep):
+            self.rep = rep
+
+        def replay(self):
+            with torch.cuda.stream(stream):
+                for inst in insts[self.rep * n_layers:(self.rep + 1) * n_layers]:
+                    fwd(inst, stream)
+
     with torch.cuda.stream(stream):
         for rep in range(REPLICAS):
             for inst in insts[rep * n_layers:(rep + 1) * n_layers]:
                 fwd(inst, stream)          # eager warm-up (sets kernel attributes)
         stream.synchronize()
         for rep in range(REPLICAS):
-            g = torch.cuda.CUDAGraph()
             c0 = QL.launch_count()
-            with torch.cuda.graph(g, stream=stream):
-                for inst in insts[rep * n_layers:(rep + 1) * n_layers]:
-                    fwd(inst, stream)
+            if eager:
+                g = EagerStep(rep)
+                g.replay()
+            else:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for inst in insts[rep * n_layers:(rep + 1) * n_layers]:
+                        fwd(inst, stream)
             launches_per_step = QL.launch_count() - c0
             graphs.append(g)
     torch.cuda.synchronize()
@@ -305,11 +322,18 @@ def main():
             for inst in group:
                 inst["layer"].forward(xr[L["d_in"]], batch, y16[L["d_out"]], flags=QL.QP_X_PREROTATED, stream=stream)
             stream.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for k in range(n_rep):
-                    group[k % REPLICAS]["layer"].forward(xr[L["d_in"]], batch, y16[L["d_out"]],
-                                                         flags=QL.QP_X_PREROTATED, stream=stream)
+            if eager:
+                def g_replay(group=group, L=L):
+                    for k in range(n_rep):
+                        group[k % REPLICAS]["layer"].forward(xr[L["d_in"]], batch, y16[L["d_out"]],
+                                                             flags=QL.QP_X_PREROTATED, stream=stream)
+                g = type("G", (), {"replay": staticmethod(g_replay)})
+            else:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for k in range(n_rep):
+                        group[k % REPLICAS]["layer"].forward(xr[L["d_in"]], batch, y16[L["d_out"]],
+                                                             flags=QL.QP_X_PREROTATED, stream=stream)
             for _ in range(3):
                 g.replay()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

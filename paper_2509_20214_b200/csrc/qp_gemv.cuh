@@ -181,13 +181,24 @@ __device__ __forceinline__ void stage_table(const uint32_t* __restrict__ g, int 
 //    A warp writes 512 contiguous bytes per STS.128 instruction (conflict-free).
 template <int REPS>
 __device__ __forceinline__ void expand_table(int words, uint8_t* tab, const uint32_t* stage) {
+  // Batches of 8 independent LDS, then 8 STS.128, so the loop runs at store bandwidth rather
+  // than at LDS latency.
   constexpr int V4 = REPS / 4;
   const int total = words * V4;
-#pragma unroll 4
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    const int e = i / V4;
-    const uint32_t v = stage[e];
-    *reinterpret_cast<uint4*>(tab + e * REPS * 4 + (i % V4) * 16) = make_uint4(v, v, v, v);
+  const int nthr = blockDim.x;
+  for (int i0 = threadIdx.x; i0 < total; i0 += 8 * nthr) {
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * nthr;
+      v[k] = i < total ? stage[i / V4] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * nthr;
+      if (i < total)
+        *reinterpret_cast<uint4*>(tab + (i / V4) * REPS * 4 + (i % V4) * 16) = make_uint4(v[k], v[k], v[k], v[k]);
+    }
   }
 }
 

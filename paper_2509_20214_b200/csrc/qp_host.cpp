@@ -68,6 +68,16 @@ void dev_free(void* p) {
   else cudaFree(p);
 }
 
+// QP_NO_PDL=1 in the environment disables programmatic dependent launch (profilers such as
+// ncu cannot replay PDL edges inside captured CUDA graphs).
+bool pdl_disabled_by_env() {
+  static const bool off = [] {
+    const char* e = getenv("QP_NO_PDL");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -584,7 +594,7 @@ qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch
   qp_status st = check_fwd_args(x, xt, batch, yt, flags);
   if (st != QP_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const bool pdl = !(flags & QP_NO_PDL);
+  const bool pdl = !(flags & QP_NO_PDL) && !pdl_disabled_by_env();
   const __half* xr = static_cast<const __half*>(x);
   void* ys[1] = {y};
   // fp32 output: the preceding kernel (rotation, or a zeroing kernel) zeroes y and CTAs that share
@@ -684,6 +694,7 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const qp_layer* l = g->cat;
   const __half* xr = static_cast<const __half*>(x);
+  if (pdl_disabled_by_env()) flags |= QP_NO_PDL;
   const bool atomic = yt == QP_F32 && !(flags & QP_DETERMINISTIC);
   long long zn[kMaxGroup];
   for (int i = 0; i < n; ++i) zn[i] = (long long)batch * g->d_outs[i];
