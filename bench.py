@@ -19,7 +19,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -64,45 +63,48 @@ def workload(world=1):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle-reason sampling DURING the timed region (B200_PROFILING.md clocks
+    line), through NVML from a background thread every 2 ms (nvidia-smi -lms into a pipe is
+    block-buffered and returned nothing for short regions)."""
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.sm, self.reasons, self.max_mhz = index, [], set(), None
+        self.stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
-                text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            masks = {k: getattr(N, v) for k, v in self.REASONS.items()}
+
+            def run():
+                while not self.stop.is_set():
+                    self.sm.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.reasons.update(k for k, m in masks.items() if r & m)
+                    time.sleep(0.002)
+            self.t = threading.Thread(target=run, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception:                      # no NVML: report no samples
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait()
+        self.stop.set()
+        if self.t:
+            self.t.join()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            for n, v in zip(names, r[3:7]):
-                if v.strip().lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 def measured_peaks():
@@ -113,14 +115,17 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def oracle_sample(layers, budget_rows=512):
-    """CPU baseline: the float64 oracle (decode + RHT + matvec) on a bounded sample."""
+def oracle_sample(layers, budget_rows=512, which=None):
+    """CPU baseline: the float64 oracle (decode + RHT + matvec) on a bounded sample: the first
+    `budget_rows` rows of every layer (or of layers[which] only)."""
     import oracle.decode as odec
     import oracle.rht as orht
     from oracle import codebooks as ocb
     from qp_synth import activations_fp16, channel_scales, random_code_bytes
     total_bytes, t0 = 0, time.perf_counter()
     for li, L in enumerate(layers):
+        if which is not None and li != which:
+            continue
         d_out, d_in, scheme, x4, tb = L["d_out"], L["d_in"], L["scheme"], L["bits_x4"], L["tb"]
         tl = np.fromfile(tlut_file(scheme, x4)[0], dtype="<f2").astype(np.float64).reshape(-1, 2)
         book = {"lut": ocb.quantlut_sym(tl, 16, tb), "L": 16}
@@ -148,25 +153,29 @@ def cpu_cores():
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the float64 oracle as it stands, on the host cores. Each step is a
+    bounded sample of the C2 workload: one 32-row tile of one layer, cycling through the 9
+    layers (so K steps stay within minutes at the default K)."""
     if rank != 0:
         return
     layers = workload(1)
-    times, nbytes = [], 0
+    times, nbytes = [], []
     for i in range(args.warmup + args.steps):
-        nb, dt = oracle_sample(layers, budget_rows=64)
+        nb, dt = oracle_sample(layers, budget_rows=32, which=i % len(layers))
         if i >= args.warmup:
             times.append(dt)
-            nbytes = nb
-    t = statistics.mean(times)
-    v = nbytes / t / 1e9
+            nbytes.append(nb)
+    t = sum(times) / len(times)
+    v = sum(nbytes) / sum(times) / 1e9
     cores = cpu_cores()
+    sample = "one 32-row tile of one C2 layer per step, cycling through the 9 layers: float64 decode + RHT + matvec"
     line = {"metric": METRIC, "value": round(v, 6), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "C2 Llama-3.1-8B shapes x TCQ 2.5/3.25/4.0, batch 1 (64-row sample per layer)",
+            "config": {"workload": "C2: Llama-3.1-8B (4096x4096, 14336x4096, 4096x14336) x TCQ-2.5 / half-TCQ-3.25 / "
+                                   "TCQ-4.0 (L=16), batch 1 (bounded CPU sample, see cpu_baseline.sample)",
                        "batch": BATCH},
-            "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": cores, "kind": "oracle",
-                             "sample": "first 64 rows of each of the 9 layers: decode + RHT + matvec, float64"},
+            "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -174,8 +183,8 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
