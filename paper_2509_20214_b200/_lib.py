@@ -14,6 +14,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libqpalette.so")
+LIB_PATH = os.environ.get("QP_LIB_PATH", LIB_PATH)   # experiments: an alternative in-tree build
 
 QP_OK = 0
 STATUS = {0: "QP_OK", 1: "QP_ERR_INVALID_ARG", 2: "QP_ERR_UNSUPPORTED_WIDTH", 3: "QP_ERR_PARTITION_MISMATCH",

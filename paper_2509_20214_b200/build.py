@@ -37,18 +37,22 @@ def _needs(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(jobs: int = 0, force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(jobs: int = 0, force: bool = False, verbose: bool = False, defines: list[str] | None = None,
+          out: str | None = None) -> str:
+    """defines / out: experimental variants (-D flags) built into a separate object dir and .so."""
+    lib_path = out or LIB
+    bdir = BUILD if not defines else BUILD + "_" + "_".join(d.replace("=", "") for d in defines)
+    os.makedirs(bdir, exist_ok=True)
     inc_nccl, lib_nccl = nccl_dirs()
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(HERE, "..", "include", "qpalette.h")]
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     common = ["-std=c++17", "-O3", "-Xcompiler", "-fPIC", "-I", inc_nccl, "-I", CSRC,
-              "-I", os.path.join(HERE, "..", "include")]
+              "-I", os.path.join(HERE, "..", "include")] + ["-D" + d for d in (defines or [])]
     cmds = []
     objs = []
     for s in srcs:
-        obj = os.path.join(BUILD, os.path.basename(s) + ".o")
+        obj = os.path.join(bdir, os.path.basename(s) + ".o")
         objs.append(obj)
         if force or _needs(obj, [s] + headers):
             if s.endswith(".cu"):
@@ -68,18 +72,20 @@ def build(jobs: int = 0, force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(jobs) as ex:
         list(ex.map(run, cmds))
-    if force or cmds or not os.path.exists(LIB):
-        link = ["nvcc", *ARCH, "-shared", "-o", LIB, *objs, "-L", lib_nccl, "-l:libnccl.so.2",
+    if force or cmds or not os.path.exists(lib_path):
+        link = ["nvcc", *ARCH, "-shared", "-o", lib_path, *objs, "-L", lib_nccl, "-l:libnccl.so.2",
                 "-Xlinker", "-rpath," + lib_nccl, "-cudart", "static"]
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed: " + " ".join(link) + "\n" + r.stdout + r.stderr)
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--jobs", type=int, default=0)
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    print(build(a.jobs, a.force, verbose=True))
+    print(build(a.jobs, a.force, verbose=True, defines=a.defines, out=a.out))

@@ -68,6 +68,14 @@ __device__ __forceinline__ uint32_t field(const uint32_t* w) {
   }
 }
 
+// (a & MASK) | c as one LOP3 (ptxas otherwise re-masks c with a second LOP3 for some masks)
+template <uint32_t MASK>
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(MASK), "r"(c));
+  return d;
+}
+
 template <int REPS>
 struct RepBits {
   static constexpr int value = REPS == 32 ? 7 : REPS == 16 ? 6 : REPS == 8 ? 5 : REPS == 4 ? 4 : REPS == 2 ? 3 : 2;
@@ -88,7 +96,7 @@ struct Dec {
       constexpr int SH = PB - (L - 1 - TB);
       constexpr uint32_t MASK = ((1u << (TB + 1)) - 1u) << PB;
       const uint32_t k = SH >= 0 ? (p << (SH >= 0 ? SH : 0)) : (p >> (SH < 0 ? -SH : 0));
-      return lds32(((k & MASK) | laneoff));
+      return lds32(and_or<MASK>(k, laneoff));
     } else if constexpr (MODE == DEC_TCQ_UNSIGNED) {
       const uint32_t win = field<J * C, L, 0, NW>(w);
       const uint32_t p = win * win + win;
@@ -171,36 +179,35 @@ __device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, u
   });
 }
 
-// 1. compact table (<= 16 KB) -> shared staging area with 128-bit loads (one round trip)
-__device__ __forceinline__ void stage_table(const uint32_t* __restrict__ g, int words, uint32_t* stage) {
-  for (int i = threadIdx.x * 4; i < words; i += blockDim.x * 4)
-    *reinterpret_cast<uint4*>(stage + i) = __ldg(reinterpret_cast<const uint4*>(g + i));
-}
-
-// 2. expand: entry e, replica r at byte e*REPS*4 + r*4 (bank = replica = lane mod REPS).
-//    A warp writes 512 contiguous bytes per STS.128 instruction (conflict-free).
-template <int REPS>
-__device__ __forceinline__ void expand_table(int words, uint8_t* tab, const uint32_t* stage) {
-  // Batches of 8 independent LDS, then 8 STS.128, so the loop runs at store bandwidth rather
-  // than at LDS latency.
-  constexpr int V4 = REPS / 4;
-  const int total = words * V4;
-  const int nthr = blockDim.x;
-  for (int i0 = threadIdx.x; i0 < total; i0 += 8 * nthr) {
-    uint32_t v[8];
+// Replicated decode table: entry e, replica r at byte e*REPS*4 + r*4 (bank = replica = lane mod
+// REPS). Built straight from the compact global table in two phases so that the table loads can
+// be issued before the first tile's code loads (they would otherwise queue behind ~40 KB per SM
+// of HBM requests) and stored once they arrive: 16-byte chunk i holds 4 replicas of entry
+// i / (REPS/4), so a warp writes 512 contiguous bytes per STS.128 (conflict-free) and the lanes
+// that need the same entry word share one L1 request.
+template <int REPS, int NT>
+struct TableBuild {
+  static constexpr int V4 = REPS / 4;
+  static constexpr int B = (kSmemTableBytes / 16 + NT - 1) / NT;   // chunks per thread (image <= 128 KB)
+  uint32_t v[B];
+  __device__ __forceinline__ void load(const uint32_t* __restrict__ g, int words) {
+    const int total = words * V4;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int i = i0 + k * nthr;
-      v[k] = i < total ? stage[i / V4] : 0u;
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int i = i0 + k * nthr;
-      if (i < total)
-        *reinterpret_cast<uint4*>(tab + (i / V4) * REPS * 4 + (i % V4) * 16) = make_uint4(v[k], v[k], v[k], v[k]);
+    for (int k = 0; k < B; ++k) {
+      const int i = threadIdx.x + k * NT;
+      v[k] = i < total ? __ldg(g + i / V4) : 0u;
     }
   }
-}
+  __device__ __forceinline__ void store(int words, uint8_t* tab) const {
+    const int total = words * V4;
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int i = threadIdx.x + k * NT;
+      if (i < total) *reinterpret_cast<uint4*>(tab + (size_t)i * 16) = make_uint4(v[k], v[k], v[k], v[k]);
+    }
+  }
+};
+
 
 __device__ __forceinline__ uint32_t owner_of(uint32_t t, uint32_t lo, uint32_t n, uint32_t parts) {
   // part p owns [lo + n*p/parts, lo + n*(p+1)/parts); returns the p that contains t
@@ -246,9 +253,6 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
   const int KH = p.KT / 2;
   const long long rowtile_bytes = (long long)KH * 512 * CLO + (long long)(KT - KH) * 512 * CHI;
 
-  uint64_t pol_keep, pol_stream;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
   auto tile_ptr = [&](uint32_t rt, int kt) -> const uint8_t* {
     const long long off = (long long)rt * rowtile_bytes + (kt < KH ? (long long)kt * 512 * CLO
                                                         : (long long)KH * 512 * CLO + (long long)(kt - KH) * 512 * CHI);
@@ -261,26 +265,14 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
     for (int i = 0; i < CMAX; ++i) {
       if (CLO == CHI || i < c) {
         uint4 v;
-        // streamed exactly once: no L1 allocation, first out of L2
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + i * 32), "l"(pol_stream));
+        // streamed exactly once: no L1 allocation (no cache-policy operand: that costs two R2UR
+        // per load in the main loop)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + i * 32));
         buf[4 * i] = v.x; buf[4 * i + 1] = v.y; buf[4 * i + 2] = v.z; buf[4 * i + 3] = v.w;
       }
     }
   };
-
-  // The compact decode table is on the critical path of the prologue: request it before the
-  // first code tiles flood the memory queues, and keep it resident in L2 across launches.
-  constexpr int kStageV4 = 4;   // <= 4 x 16 B per thread: tables up to 32 KB with 512 threads
-  uint4 tstage[kStageV4];
-#pragma unroll
-  for (int k = 0; k < kStageV4; ++k) {
-    const int i = (threadIdx.x + k * NWARP * 32) * 4;
-    if (i < p.table_words)
-      asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                   : "=r"(tstage[k].x), "=r"(tstage[k].y), "=r"(tstage[k].z), "=r"(tstage[k].w)
-                   : "l"(p.table + i), "l"(pol_keep));
-  }
 
   uint32_t cur[4 * CMAX], nxt[4 * CMAX];
   uint32_t rt = a / KT;
@@ -304,21 +296,16 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
   for (int i = 0; i < 32; ++i) xb[i] = 0u;
   const bool xrow = !DEQ && g < p.batch;           // this lane holds a batch row of x'
   const __half* xlane = p.x + (size_t)g * p.d_in + 64 * q;
-  // Everything above and the table build read only immutable layer data, so under programmatic
-  // dependent launch they overlap the previous kernel (the activation rotation). x' and y are
-  // touched only after the wait.
-#pragma unroll
-  for (int k = 0; k < kStageV4; ++k) {
-    const int i = (threadIdx.x + k * NWARP * 32) * 4;
-    if (i < p.table_words) *reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(part) + i) = tstage[k];
+  // Everything up to griddepcontrol.wait reads only immutable layer data, so under programmatic
+  // dependent launch it may overlap the previous kernel. Order: table words (small, L2-resident),
+  // then the first tile's codes (HBM), then the table stores while the codes are in flight.
+  {
+    TableBuild<REPS, NWARP * 32> tb;
+    tb.load(p.table, p.table_words);
+    if (a < b) load_tile(ptr, kt, cur);
+    stamp(7);
+    tb.store(p.table_words, tab);
   }
-  __syncthreads();
-  stamp(7);
-  // first tile's codes: issued once the table has arrived (so the table request did not queue
-  // behind ~10 MB of code requests), they land while the table is expanded. Codes are immutable:
-  // safe before the PDL wait.
-  if (a < b) load_tile(ptr, kt, cur);
-  expand_table<REPS>(p.table_words, tab, reinterpret_cast<const uint32_t*>(part));
   stamp(6);
 #pragma unroll
   for (int k = 0; k < SC_PER_THREAD; ++k) {
@@ -374,6 +361,20 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
               const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
               if (bb < p.batch) store_out(p, (int)rt, row, bb, acc[m][r], scale_of(rt, row));
             }
+        } else if (p.y_atomic) {
+          // y was zeroed by the preceding kernel: add this warp's scaled partial straight into it
+          // (fire-and-forget RED.ADD.F32; no shared-memory reduction, no barrier)
+          int i = 0;
+#pragma unroll 1
+          while (i + 1 < p.n_out && (int)rt >= p.rt_begin[i + 1]) ++i;
+          float* yb = reinterpret_cast<float*>(p.y[i]) + (rt - p.rt_begin[i]) * kTileRows;
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
+              if (bb < p.batch) atomicAdd(yb + (size_t)bb * p.ldy[i] + row, acc[m][r] * scale_of(rt, row));
+            }
         } else {
           float* slot = part + (warp * 2 + (rt == a_rt ? 0 : 1)) * 256;
 #pragma unroll
@@ -392,15 +393,25 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
     }
     kt = kt_n; rt = rt_n; ptr = ptr_n;
   };
+#ifdef QP_PINGPONG
+  // two tiles per iteration with the buffers' roles swapped: no register copies
+  uint32_t t = a;
+  for (; t + 1 < b; t += 2) {
+    process(t, cur, nxt);
+    process(t + 1, nxt, cur);
+  }
+  if (t < b) process(t, cur, nxt);
+#else
   for (uint32_t t = a; t < b; ++t) {
     process(t, cur, nxt);
 #pragma unroll
     for (int i = 0; i < 4 * CMAX; ++i) cur[i] = nxt[i];
   }
+#endif
   stamp(2);
   asm volatile("griddepcontrol.launch_dependents;");
   if constexpr (DEQ) return;
-  if (nC <= 0) return;
+  if (nC <= 0 || p.y_atomic) return;
 
   // ---- reduction of the warp partials: one warp per row tile, no CTA-wide barrier in the loop ----
   __syncthreads();
@@ -524,7 +535,7 @@ int tune_nwarp();   // QP_NWARP environment override (tuning experiments), 0 = d
 template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool TUNE = false>
 struct GemvVariant {
   static constexpr int CMAX = CLO > CHI ? CLO : CHI;
-  static constexpr int NWARP = CMAX <= 6 ? 16 : 12;
+  static constexpr int NWARP = CMAX <= 6 ? 16 : 12;   // register budget
   static cudaError_t launch(const GemvParams& prm, int grid, int /*nwarps*/, bool dequant, bool pdl, cudaStream_t s) {
     if (dequant) return launch_nw<MODE, CLO, CHI, L, TB, REPS, true, NWARP>(prm, grid, pdl, s);
     if constexpr (TUNE) {

@@ -306,8 +306,18 @@ qp_status run_rht(const qp_rht* r, const void* x, qp_dtype xt, int batch, __half
   return QP_OK;
 }
 
+// CTAs of the zeroing kernel: one per 64 KB of fp32 output, 1..8
+int zero_ctas(const long long* zn, int n) {
+  long long bytes = 0;
+  for (int i = 0; i < n; ++i) bytes += zn[i] * 4;
+  return (int)std::max<long long>(1, std::min<long long>(8, (bytes + 65535) / 65536));
+}
+
+// side_ctas: CTAs of the preceding rotation / zeroing kernel. Under PDL the GEMV (one CTA per SM,
+// the whole register file) cannot share an SM with them, so a GEMV CTA placed there would start
+// its prologue only after they exit and finish last; the GEMV leaves those SMs to them instead.
 qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, const int* rt_begin, void* const* ys,
-                   const int* ldy, qp_dtype yt, bool pdl, cudaStream_t s, bool y_atomic) {
+                   const int* ldy, qp_dtype yt, bool pdl, cudaStream_t s, bool y_atomic, int side_ctas = 0) {
   GemvParams p{};
   p.y_atomic = y_atomic ? 1 : 0;
   p.codes = l->d_codes;
@@ -332,16 +342,18 @@ qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, co
   static unsigned long long* d_tl = nullptr;
   if (tl && !d_tl) { cudaMalloc(&d_tl, 4096 * 128 * 8); cudaMemset(d_tl, 0, 4096 * 128 * 8); }
   p.timeline = tl ? d_tl : nullptr;
-  cudaError_t e = l->launcher(p, l->grid, 0, false, pdl, s);
+  int grid = l->grid;
+  if (pdl && side_ctas > 0 && side_ctas <= kMaxSideCtas) grid = std::max(1, std::min(grid, num_sms() - side_ctas));
+  cudaError_t e = l->launcher(p, grid, 0, false, pdl, s);
   if (e != cudaSuccess) return cuda_fail(e, "fused dequant-GEMV launch");
   count_launch();
   if (tl) {
-    std::vector<unsigned long long> h(l->grid * 128, 0ull);
+    std::vector<unsigned long long> h(grid * 128, 0ull);
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), d_tl, h.size() * 8, cudaMemcpyDeviceToHost);
     double av[8] = {0}, mx[8] = {0};
     int cnt[8] = {0};
-    for (int c = 0; c < l->grid; ++c) {
+    for (int c = 0; c < grid; ++c) {
       unsigned long long st = ~0ull;
       for (int w = 0; w < 16; ++w) if (h[(c * 16 + w) * 8]) st = std::min(st, h[(c * 16 + w) * 8]);
       for (int k = 1; k < 8; ++k) {
@@ -356,6 +368,7 @@ qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, co
     fprintf(stderr, "kcyc (avg/max over CTAs):");
     const char* nm[8] = {"", "table", "mainend", "epiend", "epistart", "afterwait", "afterexpand", "afterstage"};
     for (int k = 1; k < 8; ++k) fprintf(stderr, " %s %.2f/%.2f", nm[k], cnt[k] ? av[k] / cnt[k] : 0.0, mx[k]);
+    fprintf(stderr, " grid %d", grid);
     fprintf(stderr, "\n");
     cudaMemset(d_tl, 0, 4096 * 128 * 8);
   }
@@ -420,6 +433,9 @@ qp_status qp_codebook_load(qp_scheme scheme, int bits_x4, int L, const void* hos
     if (cb->tb == 9) {
       // pre-signed key table: key = sign * 2^tb + idx -> (sign ? -t0 : t0, t1)
       cb->mode = DEC_TCQ_PRESIGNED;
+      // 32 replicas (bank = lane, conflict-free). 16 replicas would save the shift of the key
+      // (one instruction per pair) but measured 5-15% slower on B200 with the 2-way bank
+      // conflicts (profiles/r1/ubench_decode_variants.txt)
       cb->reps = 32;
       words.resize(2 * n);
       for (int sgn = 0; sgn < 2; ++sgn)
@@ -601,20 +617,23 @@ qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch
   // a row tile add into it; QP_DETERMINISTIC or fp16 output: in-order cross-CTA reduction instead
   const bool atomic = yt == QP_F32 && !(flags & QP_DETERMINISTIC);
   const long long zn[1] = {(long long)batch * l->d_out};
+  int side = 0;
   if (!(flags & QP_X_PREROTATED)) {
     if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, pdl, s, atomic ? 1 : 0, ys, zn)) != QP_OK) return st;
     xr = l->d_xrot;
+    side = batch * (l->d_in / l->rht->block);
   } else if (atomic) {
     RhtParams zp{};
     zp.n_zero = 1;
     zp.zero_ptr[0] = static_cast<float*>(y);
     zp.zero_n[0] = zn[0];
-    cudaError_t e = launch_zero(zp, pdl, s);
+    side = zero_ctas(zn, 1);
+    cudaError_t e = launch_zero(zp, side, pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "zero kernel launch");
   }
   const int rtb[2] = {0, l->d_out / kTileRows};
   const int ldy[1] = {l->d_out};
-  return run_gemv(l, xr, batch, 1, rtb, ys, ldy, yt, pdl, s, atomic);
+  return run_gemv(l, xr, batch, 1, rtb, ys, ldy, yt, pdl, s, atomic, side);
 }
 
 qp_status qp_dequantize(const qp_layer* l, void* W_hat_fp16, void* stream) {
@@ -698,9 +717,11 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
   const bool atomic = yt == QP_F32 && !(flags & QP_DETERMINISTIC);
   long long zn[kMaxGroup];
   for (int i = 0; i < n; ++i) zn[i] = (long long)batch * g->d_outs[i];
+  int side = 0;
   if (!(flags & QP_X_PREROTATED)) {
     if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, !(flags & QP_NO_PDL), s, atomic ? n : 0, ys, zn)) != QP_OK) return st;
     xr = l->d_xrot;
+    side = batch * (l->d_in / l->rht->block);
   } else if (atomic) {
     RhtParams zp{};
     zp.n_zero = n;
@@ -708,7 +729,8 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
       zp.zero_ptr[i] = static_cast<float*>(ys[i]);
       zp.zero_n[i] = zn[i];
     }
-    cudaError_t e = launch_zero(zp, !(flags & QP_NO_PDL), s);
+    side = zero_ctas(zn, n);
+    cudaError_t e = launch_zero(zp, side, !(flags & QP_NO_PDL), s);
     if (e != cudaSuccess) return cuda_fail(e, "zero kernel launch");
   }
   int rtb[kMaxGroup + 1];
@@ -718,7 +740,7 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
     rtb[i + 1] = rtb[i] + g->d_outs[i] / kTileRows;
     ldy[i] = g->d_outs[i];
   }
-  return run_gemv(l, xr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic);
+  return run_gemv(l, xr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic, side);
 }
 
 qp_status qp_layer_shard(const qp_layer* l, int rank, int world, qp_layer** out) {

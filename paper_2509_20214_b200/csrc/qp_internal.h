@@ -20,6 +20,7 @@ constexpr int kMaxGroup = 8;        // members of a fused group
 constexpr int kTileRows = 32;
 constexpr int kTileCols = 256;
 constexpr int kSmemTableBytes = 131072;
+constexpr int kMaxSideCtas = 16;   // preceding-kernel CTAs the GEMV grid steps aside for (run_gemv)
 
 // Static description of one kernel variant.
 struct KernelKey {
@@ -81,7 +82,7 @@ void register_gemv(const KernelKey& k, GemvLauncher f);
 int gemv_smem_bytes(int nwarps);
 
 cudaError_t launch_rht(const RhtParams& p, bool pdl, cudaStream_t s);
-cudaError_t launch_zero(const RhtParams& p, bool pdl, cudaStream_t s);   // only the n_zero/zero_* fields
+cudaError_t launch_zero(const RhtParams& p, int grid, bool pdl, cudaStream_t s);   // only the n_zero/zero_* fields
 cudaError_t launch_gather_permute(const void* src, void* dst, int world, int batch, int m, int elem_bytes,
                                   cudaStream_t s);
 void count_launch();

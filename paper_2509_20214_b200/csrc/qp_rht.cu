@@ -154,10 +154,10 @@ cudaError_t launch_rht(const RhtParams& p, bool pdl, cudaStream_t s) {
   return e;
 }
 
-cudaError_t launch_zero(const RhtParams& p, bool pdl, cudaStream_t s) {
+cudaError_t launch_zero(const RhtParams& p, int grid, bool pdl, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(64);
-  cfg.blockDim = dim3(256);
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(1024);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

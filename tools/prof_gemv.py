@@ -24,6 +24,8 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--replicas", type=int, default=4)
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--pdl", action="store_true")
+ap.add_argument("--rht", action="store_true", help="forward from raw x (rotation kernel + GEMV)")
+ap.add_argument("--y16", action="store_true", help="fp16 y (in-order cross-CTA reduction, no zeroing kernel)")
 a = ap.parse_args()
 d_out, d_in = map(int, a.shape.split("x"))
 cb = QL.Codebook(a.scheme, a.bits_x4, Q.load_fp16(a.scheme, a.bits_x4), L=16)
@@ -34,23 +36,25 @@ lays = [QL.Layer.from_codes(random_code_bytes(Q.code_bytes(d_out, d_in, a.scheme
 x = torch.from_numpy(activations_fp16(a.batch, d_in)).cuda()
 xr = torch.empty_like(x)
 r.apply(x, a.batch, xr)
-y = torch.empty(a.batch, d_out, device="cuda")
+y = torch.empty(a.batch, d_out, device="cuda", dtype=torch.float16 if a.y16 else torch.float32)
+xin = x if a.rht else xr
+base = 0 if a.rht else QL.QP_X_PREROTATED
 for i in range(a.iters):
-    lays[i % a.replicas].forward(xr, a.batch, y, flags=QL.QP_X_PREROTATED | QL.QP_NO_PDL)
+    lays[i % a.replicas].forward(xin, a.batch, y, flags=base | QL.QP_NO_PDL)
 torch.cuda.synchronize()
 if a.time:
     # back-to-back launches captured in one CUDA graph (no host gaps), replicas cycle through L2
     stream = torch.cuda.Stream()
     n = 40
-    flags = QL.QP_X_PREROTATED | (0 if a.pdl else QL.QP_NO_PDL)
+    flags = base | (0 if a.pdl else QL.QP_NO_PDL)
     with torch.cuda.stream(stream):
         for i in range(n):
-            lays[i % a.replicas].forward(xr, a.batch, y, flags=flags, stream=stream)
+            lays[i % a.replicas].forward(xin, a.batch, y, flags=flags, stream=stream)
         stream.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             for i in range(n):
-                lays[i % a.replicas].forward(xr, a.batch, y, flags=flags, stream=stream)
+                lays[i % a.replicas].forward(xin, a.batch, y, flags=flags, stream=stream)
     import time
     t_end = time.time() + 0.3
     while time.time() < t_end:
@@ -66,5 +70,5 @@ if a.time:
     torch.cuda.synchronize()
     us = ev[0].elapsed_time(ev[1]) / (reps * n) * 1e3
     nbytes = lays[0].code_bytes
-    print(f"{a.shape} {a.scheme} {a.bits_x4/4}b batch {a.batch} (graph, pdl={a.pdl}): {us:.2f} us/launch "
-          f"(incl. zero kernel), codes {nbytes/us/1e3:.1f} GB/s = {nbytes/us/1e3/6535*100:.1f}% of 6535")
+    print(f"{a.shape} {a.scheme} {a.bits_x4/4}b batch {a.batch} (graph, pdl={a.pdl}, rht={a.rht}, y16={a.y16}): {us:.2f} us/launch "
+          f"(incl. rotation or zero kernel), codes {nbytes/us/1e3:.1f} GB/s = {nbytes/us/1e3/6535*100:.1f}% of 6535")
