@@ -107,6 +107,23 @@ class Clocks:
                 "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
+def ncu_traffic(layers, batch):
+    """DRAM bytes (read + write) per GEMV launch, averaged over the step's layers, from the
+    committed ncu capture (profiles/gemv_traffic.json, written by tools/ncu_traffic.py --parse);
+    None if that capture does not cover this workload."""
+    p = os.path.join(ROOT, "profiles", "gemv_traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    d = json.load(open(p))
+    vals = []
+    for L in layers:
+        k = f'{L["m"]}x{L["d_in"]}:{L["scheme"]}:{L["bits_x4"]}:b{batch}'
+        if k not in d["layers"]:
+            return None, None
+        vals.append(d["layers"][k]["dram_bytes"])
+    return sum(vals) / len(vals), d.get("source")
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -321,7 +338,9 @@ def main():
         if d_in not in xr:
             xr[d_in] = torch.empty(batch, d_in, dtype=torch.float16, device=dev)
             rots[d_in].apply(inst["x"], batch, xr[d_in])
-    y16 = {L["d_out"]: torch.empty(batch, L["m"], dtype=torch.float16, device=dev) for L in layers}
+    # fp32 y with QP_Y_ACCUMULATE: exactly one kernel (the fused GEMV) per launch, no zeroing
+    yacc = {L["d_out"]: torch.zeros(batch, L["m"], dtype=torch.float32, device=dev) for L in layers}
+    kflags = QL.QP_X_PREROTATED | QL.QP_Y_ACCUMULATE
     torch.cuda.synchronize()
     per_layer_us, gemv_time_s, gemv_alg = {}, 0.0, 0
     n_rep = 8
@@ -329,20 +348,20 @@ def main():
         group = [insts[rep * n_layers + li] for rep in range(REPLICAS)]
         with torch.cuda.stream(stream):
             for inst in group:
-                inst["layer"].forward(xr[L["d_in"]], batch, y16[L["d_out"]], flags=QL.QP_X_PREROTATED, stream=stream)
+                inst["layer"].forward(xr[L["d_in"]], batch, yacc[L["d_out"]], flags=kflags, stream=stream)
             stream.synchronize()
             if eager:
                 def g_replay(group=group, L=L):
                     for k in range(n_rep):
-                        group[k % REPLICAS]["layer"].forward(xr[L["d_in"]], batch, y16[L["d_out"]],
-                                                             flags=QL.QP_X_PREROTATED, stream=stream)
+                        group[k % REPLICAS]["layer"].forward(xr[L["d_in"]], batch, yacc[L["d_out"]],
+                                                             flags=kflags, stream=stream)
                 g = type("G", (), {"replay": staticmethod(g_replay)})
             else:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
                     for k in range(n_rep):
-                        group[k % REPLICAS]["layer"].forward(xr[L["d_in"]], batch, y16[L["d_out"]],
-                                                             flags=QL.QP_X_PREROTATED, stream=stream)
+                        group[k % REPLICAS]["layer"].forward(xr[L["d_in"]], batch, yacc[L["d_out"]],
+                                                             flags=kflags, stream=stream)
             for _ in range(3):
                 g.replay()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -355,10 +374,11 @@ def main():
         us = a.elapsed_time(b) * 1e3 / (reps * n_rep)
         per_layer_us[f'{L["d_out"]}x{L["d_in"]}@{L["bits_x4"] / 4:g}b'] = round(us, 3)
         gemv_time_s += us * 1e-6
-        gemv_alg += layer_bytes(L["m"], L["d_in"], L["bits_x4"], L["tb"], batch)[0] - 2 * batch * L["m"]
-    gemv_achieved = gemv_alg / gemv_time_s / 1e9          # fp16 y: 2 bytes per output, not 4
+        gemv_alg += layer_bytes(L["m"], L["d_in"], L["bits_x4"], L["tb"], batch)[0]
+    gemv_achieved = gemv_alg / gemv_time_s / 1e9
     gemv_avg_ms = gemv_time_s / n_layers * 1e3
     peak, peak_kind = measured_peaks()
+    traffic, traffic_src = ncu_traffic(layers, batch)
 
     # ---- end to end through the public API with host buffers (N=1 only) ------------------
     e2e = None
@@ -408,7 +428,9 @@ def main():
                        "graph": "CUDA graph per step, PDL between the rotation and GEMV kernels",
                        "gemv_us_per_layer": per_layer_us},
             "roofline": {"bound": "hbm", "achieved": round(gemv_achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(gemv_achieved / peak, 4), "traffic": None,
+                         "frac": round(gemv_achieved / peak, 4),
+                         "traffic": round(traffic) if traffic else None, "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": round(gemv_alg / n_layers),
                          "kernel": "qp_gemv_kernel (fused dequant-GEMV), all 9 layers, CUDA graph of back-to-back "
                                    "launches per layer, events on the launching stream",
                          "peak_kind": peak_kind, "avg_launch_us": round(gemv_avg_ms * 1e3, 3)},

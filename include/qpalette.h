@@ -73,6 +73,8 @@ typedef enum { QP_F16 = 0, QP_BF16 = 1, QP_F32 = 2 } qp_dtype;
 #define QP_NO_PDL 2u         /* launch without programmatic dependent launch        */
 #define QP_DETERMINISTIC 4u  /* fp32 y: in-order cross-CTA reduction (bitwise reproducible) instead of
                                 zero-then-atomic-add (fp16 y is always in-order)        */
+#define QP_Y_ACCUMULATE 8u  /* fp32 y only: y += diag(s) W_hat R x (y is not zeroed first; e.g. a residual
+                                add). Not with QP_DETERMINISTIC.                                        */
 
 typedef struct qp_codebook qp_codebook;
 typedef struct qp_rht qp_rht;
@@ -141,6 +143,16 @@ qp_status qp_dequantize(const qp_layer* l, void* W_hat_fp16, void* stream);
 /* Contiguous row block [rank*d_out/world, (rank+1)*d_out/world) of a layer as a new
  * layer (device copy). (d_out/world) % 32 must be 0. */
 qp_status qp_layer_shard(const qp_layer* l, int rank, int world, qp_layer** out);
+
+/* Host-only (no device work, usable without a GPU): where rank `rank` of `world` finds its row
+ * shard of a (d_out x d_in, scheme, bits_x4) layer: rows [*row0, *row0 + *rows) and code bytes
+ * [*byte0, *byte0 + *nbytes) of the LAYOUT.md stream (row-tile-major, so a row block is one
+ * contiguous byte range). The all-gather of qp_linear_fwd_sharded concatenates the ranks' rows in
+ * rank order. Errors: QP_ERR_INVALID_ARG (NULL / rank outside [0, world)),
+ * QP_ERR_UNSUPPORTED_WIDTH, QP_ERR_PARTITION_MISMATCH (d_out % world, (d_out/world) % 32, or the
+ * layer's own partition rules). */
+qp_status qp_shard_range(int d_out, int d_in, qp_scheme scheme, int bits_x4, int rank, int world, int* row0,
+                         int* rows, size_t* byte0, size_t* nbytes);
 
 /* NCCL plumbing for the row-sharded path (NCCL over NVLink / NVSwitch).
  * qp_nccl_unique_id writes 128 bytes; broadcast them (e.g. with torch.distributed)

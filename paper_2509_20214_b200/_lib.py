@@ -25,6 +25,7 @@ DTYPES = {"f16": 0, "bf16": 1, "f32": 2}
 QP_X_PREROTATED = 1
 QP_NO_PDL = 2
 QP_DETERMINISTIC = 4
+QP_Y_ACCUMULATE = 8
 
 # every symbol include/qpalette.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -32,7 +33,7 @@ EXPORTS = [
     "qp_layer_from_codes", "qp_quantize_offline", "qp_layer_get_codes", "qp_layer_get_scales", "qp_linear_fwd",
     "qp_fuse", "qp_group_free", "qp_fused_linear", "qp_dequantize", "qp_layer_shard", "qp_nccl_unique_id",
     "qp_nccl_comm_create", "qp_nccl_comm_destroy", "qp_linear_fwd_sharded", "qp_layer_info", "qp_launch_count",
-    "qp_layer_free", "qp_last_error", "qp_version",
+    "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range",
 ]
 
 
@@ -69,6 +70,7 @@ def lib() -> C.CDLL:
             "qp_fused_linear": [vp, vp, i, i, C.POINTER(vp), i, C.c_uint, vp],
             "qp_dequantize": [vp, vp, vp],
             "qp_layer_shard": [vp, i, i, C.POINTER(vp)],
+            "qp_shard_range": [i, i, i, i, i, i, C.POINTER(i), C.POINTER(i), C.POINTER(sz), C.POINTER(sz)],
             "qp_nccl_unique_id": [vp],
             "qp_nccl_comm_create": [vp, i, i, C.POINTER(vp)],
             "qp_nccl_comm_destroy": [vp],
@@ -114,6 +116,14 @@ def _stream(stream) -> int:
 def _dtype_code(t) -> int:
     import torch
     return {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2}[t.dtype]
+
+
+def shard_range(d_out: int, d_in: int, scheme: str, bits_x4: int, rank: int, world: int):
+    """(row0, rows, byte0, nbytes) of rank's row shard (qp_shard_range; host-only, no GPU)."""
+    r0, n, b0, nb = C.c_int(), C.c_int(), C.c_size_t(), C.c_size_t()
+    check(lib().qp_shard_range(d_out, d_in, SCHEMES[scheme], bits_x4, rank, world, C.byref(r0), C.byref(n),
+                               C.byref(b0), C.byref(nb)))
+    return r0.value, n.value, b0.value, nb.value
 
 
 class Codebook:

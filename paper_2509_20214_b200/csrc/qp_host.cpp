@@ -383,6 +383,8 @@ qp_status check_fwd_args(const void* x, qp_dtype xt, int batch, qp_dtype yt, uns
     return fail(QP_ERR_INVALID_ARG, "dtype: x in {F16,BF16,F32}, y in {F16,F32}");
   if ((flags & QP_X_PREROTATED) && xt != QP_F16)
     return fail(QP_ERR_INVALID_ARG, "QP_X_PREROTATED requires fp16 x (the output dtype of qp_rht_apply)");
+  if ((flags & QP_Y_ACCUMULATE) && (yt != QP_F32 || (flags & QP_DETERMINISTIC)))
+    return fail(QP_ERR_INVALID_ARG, "QP_Y_ACCUMULATE needs fp32 y and excludes QP_DETERMINISTIC");
   return QP_OK;
 }
 
@@ -619,10 +621,11 @@ qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch
   const long long zn[1] = {(long long)batch * l->d_out};
   int side = 0;
   if (!(flags & QP_X_PREROTATED)) {
-    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, pdl, s, atomic ? 1 : 0, ys, zn)) != QP_OK) return st;
+    const int nz = atomic && !(flags & QP_Y_ACCUMULATE) ? 1 : 0;
+    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, pdl, s, nz, ys, zn)) != QP_OK) return st;
     xr = l->d_xrot;
     side = batch * (l->d_in / l->rht->block);
-  } else if (atomic) {
+  } else if (atomic && !(flags & QP_Y_ACCUMULATE)) {
     RhtParams zp{};
     zp.n_zero = 1;
     zp.zero_ptr[0] = static_cast<float*>(y);
@@ -719,10 +722,11 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
   for (int i = 0; i < n; ++i) zn[i] = (long long)batch * g->d_outs[i];
   int side = 0;
   if (!(flags & QP_X_PREROTATED)) {
-    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, !(flags & QP_NO_PDL), s, atomic ? n : 0, ys, zn)) != QP_OK) return st;
+    const int nz = atomic && !(flags & QP_Y_ACCUMULATE) ? n : 0;
+    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, !(flags & QP_NO_PDL), s, nz, ys, zn)) != QP_OK) return st;
     xr = l->d_xrot;
     side = batch * (l->d_in / l->rht->block);
-  } else if (atomic) {
+  } else if (atomic && !(flags & QP_Y_ACCUMULATE)) {
     RhtParams zp{};
     zp.n_zero = n;
     for (int i = 0; i < n; ++i) {
@@ -743,14 +747,32 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
   return run_gemv(l, xr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic, side);
 }
 
+qp_status qp_shard_range(int d_out, int d_in, qp_scheme scheme, int bits_x4, int rank, int world, int* row0,
+                         int* rows, size_t* byte0, size_t* nbytes) {
+  if (!row0 || !rows || !byte0 || !nbytes) return fail(QP_ERR_INVALID_ARG, "NULL output pointer to qp_shard_range");
+  if (world < 1 || rank < 0 || rank >= world) return fail(QP_ERR_INVALID_ARG, "rank %d / world %d", rank, world);
+  if (!width_ok(scheme, bits_x4)) return fail(QP_ERR_UNSUPPORTED_WIDTH, "unsupported width %.2f", bits_x4 / 4.0);
+  qp_status st = check_shape(scheme, bits_x4, d_out, d_in);
+  if (st != QP_OK) return st;
+  if (d_out % world || (d_out / world) % kTileRows)
+    return fail(QP_ERR_PARTITION_MISMATCH, "d_out=%d does not split into %d row blocks of a multiple of 32", d_out,
+                world);
+  const int m = d_out / world;
+  const size_t shard_bytes = layout_bytes(scheme, bits_x4, m, d_in);
+  *row0 = rank * m;
+  *rows = m;
+  *byte0 = (size_t)rank * shard_bytes;
+  *nbytes = shard_bytes;
+  return QP_OK;
+}
+
 qp_status qp_layer_shard(const qp_layer* l, int rank, int world, qp_layer** out) {
   if (!l || !out) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_layer_shard");
   *out = nullptr;
-  if (world < 1 || rank < 0 || rank >= world) return fail(QP_ERR_INVALID_ARG, "rank %d / world %d", rank, world);
-  if (l->d_out % world || (l->d_out / world) % kTileRows)
-    return fail(QP_ERR_PARTITION_MISMATCH, "d_out=%d does not split into %d row blocks of a multiple of 32", l->d_out,
-                world);
-  const int m = l->d_out / world;
+  int row0 = 0, m = 0;
+  size_t byte0 = 0, nb = 0;
+  qp_status rs = qp_shard_range(l->d_out, l->d_in, l->scheme, l->bits_x4, rank, world, &row0, &m, &byte0, &nb);
+  if (rs != QP_OK) return rs;
   auto s = new qp_layer();
   qp_status st = layer_init(s, m, l->d_in, l->scheme, l->bits_x4, l->cb, l->rht);
   if (st != QP_OK) {
@@ -759,10 +781,9 @@ qp_status qp_layer_shard(const qp_layer* l, int rank, int world, qp_layer** out)
     return st;
   }
   // row-tile-major storage: rows [rank*m, (rank+1)*m) are one contiguous byte range (LAYOUT.md)
-  cudaError_t e = cudaMemcpy(s->d_codes, l->d_codes + (size_t)rank * s->code_bytes, s->code_bytes,
-                             cudaMemcpyDeviceToDevice);
+  cudaError_t e = cudaMemcpy(s->d_codes, l->d_codes + byte0, nb, cudaMemcpyDeviceToDevice);
   if (e == cudaSuccess)
-    e = cudaMemcpy(s->d_scales, l->d_scales + (size_t)rank * m, (size_t)m * 4, cudaMemcpyDeviceToDevice);
+    e = cudaMemcpy(s->d_scales, l->d_scales + row0, (size_t)m * 4, cudaMemcpyDeviceToDevice);
   if (e != cudaSuccess) {
     layer_release(s);
     delete s;

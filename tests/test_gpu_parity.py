@@ -303,3 +303,27 @@ def test_offline_rtn_matches_oracle(scheme, bits_x4):
     codes_o, s_o = linear.quantize_offline(W.astype(np.float64), scheme, bits_x4, ocb, SEED)
     assert np.allclose(lay.scales(), s_o, rtol=1e-6)
     assert np.mean(lay.codes() == codes_o) > 0.99
+
+
+def test_y_accumulate_flag():
+    """QP_Y_ACCUMULATE: y += diag(s) W_hat R x on fp32 y (no zeroing), with and without the
+    rotation kernel; rejected for fp16 y and with QP_DETERMINISTIC."""
+    Lb = _need_gpu()
+    lay, codes, s, ocb = _layer("tcq", 10, 1024, 2048, layer_id=21)
+    x = activations_fp16(3, 2048)
+    y_ref = linear.linear_from_codes(codes, 1024, 2048, "tcq", 10, ocb, s, x.astype(np.float64), SEED)
+    y0 = np.random.default_rng(5).standard_normal((3, 1024)).astype(np.float32)
+    xg = torch.from_numpy(x).cuda()
+    r = _rht(2048)
+    xr = torch.empty(3, 2048, dtype=torch.float16, device="cuda")
+    r.apply(xg, 3, xr)
+    for xin, fl in ((xg, 0), (xr, Lb.QP_X_PREROTATED)):
+        y = torch.from_numpy(y0.copy()).cuda()
+        lay.forward(xin, 3, y, flags=fl | Lb.QP_Y_ACCUMULATE)
+        torch.cuda.synchronize()
+        got = y.cpu().numpy() - y0
+        assert np.max(linear.normwise_error(got, y_ref)) <= TOL
+    with pytest.raises(Lb.QPError):
+        lay.forward(xg, 3, torch.empty(3, 1024, dtype=torch.float16, device="cuda"), flags=Lb.QP_Y_ACCUMULATE)
+    with pytest.raises(Lb.QPError):
+        lay.forward(xg, 3, torch.empty(3, 1024, device="cuda"), flags=Lb.QP_Y_ACCUMULATE | Lb.QP_DETERMINISTIC)
