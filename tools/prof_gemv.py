@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2509_20214_b200 import _lib as QL  # noqa: E402
 from qp_synth import activations_fp16, channel_scales, random_code_bytes  # noqa: E402
-from tests import qp_cases as Q  # noqa: E402
+from tools import palette as Q  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="14336x4096")
