@@ -154,6 +154,15 @@ qp_status qp_layer_shard(const qp_layer* l, int rank, int world, qp_layer** out)
 qp_status qp_shard_range(int d_out, int d_in, qp_scheme scheme, int bits_x4, int rank, int world, int* row0,
                          int* rows, size_t* byte0, size_t* nbytes);
 
+/* Host-only (no device work): Theorem 1 of the paper, the optimal fractional bit
+ * allocation with ideal Gaussian quantizers for L layers with sensitivities a[l] > 0 and sizes
+ * n[l] = d_in * d_out > 0 (weights) under a total budget of M bits and a floor eta:
+ *     b_out[l] = max{eta, ln(a[l] / n[l]) / (2 ln 2) + C},  C such that sum_l b_out[l] n[l] = M.
+ * Exact (sorted breakpoints, no iteration). The caller owns all arrays (length L).
+ * Errors: QP_ERR_INVALID_ARG (NULL, L <= 0, non-positive a / n, eta < 0),
+ * QP_ERR_CONFIG_MISMATCH (infeasible: M < eta * sum n). */
+qp_status qp_optimal_bits(const double* a, const double* n, int L, double M, double eta, double* b_out);
+
 /* NCCL plumbing for the row-sharded path (NCCL over NVLink / NVSwitch).
  * qp_nccl_unique_id writes 128 bytes; broadcast them (e.g. with torch.distributed)
  * and call qp_nccl_comm_create on every rank. comm is an ncclComm_t. */

@@ -33,7 +33,7 @@ EXPORTS = [
     "qp_layer_from_codes", "qp_quantize_offline", "qp_layer_get_codes", "qp_layer_get_scales", "qp_linear_fwd",
     "qp_fuse", "qp_group_free", "qp_fused_linear", "qp_dequantize", "qp_layer_shard", "qp_nccl_unique_id",
     "qp_nccl_comm_create", "qp_nccl_comm_destroy", "qp_linear_fwd_sharded", "qp_layer_info", "qp_launch_count",
-    "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range",
+    "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range", "qp_optimal_bits",
 ]
 
 
@@ -71,6 +71,8 @@ def lib() -> C.CDLL:
             "qp_dequantize": [vp, vp, vp],
             "qp_layer_shard": [vp, i, i, C.POINTER(vp)],
             "qp_shard_range": [i, i, i, i, i, i, C.POINTER(i), C.POINTER(i), C.POINTER(sz), C.POINTER(sz)],
+            "qp_optimal_bits": [C.POINTER(C.c_double), C.POINTER(C.c_double), i, C.c_double, C.c_double,
+                                C.POINTER(C.c_double)],
             "qp_nccl_unique_id": [vp],
             "qp_nccl_comm_create": [vp, i, i, C.POINTER(vp)],
             "qp_nccl_comm_destroy": [vp],
@@ -261,3 +263,14 @@ class NcclComm:
         if getattr(self, "h", None):
             check(lib().qp_nccl_comm_destroy(self.h))
             self.h = None
+
+
+def optimal_bits(a, n, M: float, eta: float) -> np.ndarray:
+    """qp_optimal_bits (host-only): Theorem 1 allocation b_l* for sensitivities a, sizes n."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    n = np.ascontiguousarray(n, dtype=np.float64)
+    out = np.empty_like(a)
+    dp = C.POINTER(C.c_double)
+    check(lib().qp_optimal_bits(a.ctypes.data_as(dp), n.ctypes.data_as(dp), len(a), float(M), float(eta),
+                                out.ctypes.data_as(dp)))
+    return out

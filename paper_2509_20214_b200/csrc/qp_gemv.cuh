@@ -6,9 +6,13 @@
 //  * persistent grid, one CTA per SM (128 KB replicated decode table in shared memory);
 //    the RT x KT tiles (32 rows x 256 cols, LAYOUT.md) are split into contiguous,
 //    k-minor ranges per CTA and per warp (flat stream-K: balanced to within one tile);
-//  * each lane owns one 256-weight trellis / code run per tile: its 4c stream words are
-//    loaded with c coalesced 128-bit loads (512 B per warp instruction), the next tile's
-//    words are prefetched while the current tile is decoded;
+//  * each lane owns one 256-weight trellis / code run per tile. A tile's codes are one
+//    contiguous 512c-byte block; every warp streams its tiles into a private NS-stage ring in
+//    shared memory with 1-D bulk-async copies (cp.async.bulk, the TMA engine; one elected lane
+//    issues them, completion on a per-stage mbarrier), NS tiles ahead of the decode, so code
+//    loads never block instruction issue (the register-prefetch design stalled the prologue's
+//    table build behind ~40 KB/SM of outstanding LDGs). Each lane then reads its 4c stream
+//    words with c conflict-free 128-bit shared loads;
 //  * decode per weight pair (TCQ): funnel-shift window -> hash (w+1)w -> masked key ->
 //    one conflict-free LDS from a 32-way replicated table (bank = lane) -> half2;
 //    VQ/NUQ/UNIF: funnel-shift index -> LDS. Pairs land directly in mma.sync m16n8k16
@@ -74,6 +78,49 @@ __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t c) {
   uint32_t d;
   asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(MASK), "r"(c));
   return d;
+}
+
+
+// ---- mbarrier + 1-D bulk async copy (TMA engine) helpers ---------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+}
+// arrive (count 1) and announce `bytes` of transaction for the current phase
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "QP_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra QP_WAIT_%=;\n}" :: "r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, 16-B aligned), completing on `bar`;
+// the codes are read exactly once: L2 evict-first.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+#ifdef QP_NO_EVICT_FIRST
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+  return;
+#endif
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
 }
 
 template <int REPS>
@@ -185,27 +232,54 @@ __device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, u
 // of HBM requests) and stored once they arrive: 16-byte chunk i holds 4 replicas of entry
 // i / (REPS/4), so a warp writes 512 contiguous bytes per STS.128 (conflict-free) and the lanes
 // that need the same entry word share one L1 request.
-template <int REPS, int NT>
+template <int REPS, int NT, int ENTRIES>
 struct TableBuild {
+  // the compact table has exactly ENTRIES words (the host pads it): no bounds predicates
   static constexpr int V4 = REPS / 4;
-  static constexpr int B = (kSmemTableBytes / 16 + NT - 1) / NT;   // chunks per thread (image <= 128 KB)
+  static constexpr int TOTAL = ENTRIES * V4;             // 16-byte chunks of the image
+  static constexpr int B = (TOTAL + NT - 1) / NT;        // chunks per thread
+  static constexpr bool EXACT = TOTAL % NT == 0;
   uint32_t v[B];
-  __device__ __forceinline__ void load(const uint32_t* __restrict__ g, int words) {
-    const int total = words * V4;
+  __device__ __forceinline__ void load(const uint32_t* __restrict__ g) {
 #pragma unroll
     for (int k = 0; k < B; ++k) {
       const int i = threadIdx.x + k * NT;
-      v[k] = i < total ? __ldg(g + i / V4) : 0u;
+      v[k] = (EXACT || k + 1 < B || i < TOTAL) ? __ldg(g + i / V4) : 0u;
     }
   }
-  __device__ __forceinline__ void store(int words, uint8_t* tab) const {
-    const int total = words * V4;
+  __device__ __forceinline__ void store(uint8_t* tab) const {
 #pragma unroll
     for (int k = 0; k < B; ++k) {
       const int i = threadIdx.x + k * NT;
-      if (i < total) *reinterpret_cast<uint4*>(tab + (size_t)i * 16) = make_uint4(v[k], v[k], v[k], v[k]);
+      if (EXACT || k + 1 < B || i < TOTAL) *reinterpret_cast<uint4*>(tab + (size_t)i * 16) = make_uint4(v[k], v[k], v[k], v[k]);
     }
   }
+};
+
+// Compile-time shared-memory plan of one kernel variant:
+//   [0, TAB)                     replicated decode table (entries x REPS x 4 B)
+//   [TAB, TAB + RING)            per-warp code rings: NWARP x NS stages x 512*CMAX bytes
+//                                (aliased by the epilogue's warp partials, used after the loop)
+//   [.., + 8*NWARP*NS)           one mbarrier per stage
+template <int MODE, int CLO, int CHI, int TB, int REPS>
+struct Plan {
+  static constexpr int CMAX = CLO > CHI ? CLO : CHI;
+  static constexpr int ENTRIES = MODE == DEC_TCQ_PRESIGNED ? (2 << TB) : MODE == DEC_LUT2 ? (1 << CLO) : (1 << TB);
+  static constexpr int TAB = ENTRIES * REPS * 4 < 4096 ? 4096 : ENTRIES * REPS * 4;
+  static constexpr int SMEM_MAX = 232448;          // sm_100 opt-in per block
+  static constexpr int STAGE = 512 * CMAX;
+  static constexpr int NW0 = CMAX <= 8 ? 16 : 12;  // register budget (128 regs x 512 threads)
+  static constexpr int ns_for(int nw) {
+    const int n = (SMEM_MAX - TAB - 1024) / (nw * STAGE);
+    return n > 4 ? 4 : n;
+  }
+  static constexpr int NWARP = ns_for(NW0) >= 1 ? NW0 : (ns_for(12) >= 1 ? 12 : 8);
+  static constexpr int NS = ns_for(NWARP);   // a stage is refilled as soon as it is read: NS tiles ahead
+  static constexpr int PART = NWARP * 2 * 256 * 4;  // epilogue warp partials
+  static constexpr int RING = NWARP * NS * STAGE > PART ? NWARP * NS * STAGE : PART;
+  static constexpr int BAR_OFF = TAB + RING;
+  static constexpr int SMEM = BAR_OFF + ((8 * NWARP * NS + 127) / 128) * 128;
+  static_assert(NS >= 1 && SMEM <= SMEM_MAX, "shared-memory plan does not fit");
 };
 
 
@@ -224,93 +298,101 @@ __device__ __forceinline__ void store_out(const GemvParams& p, int rt, int row, 
   else reinterpret_cast<__half*>(p.y[i])[(size_t)b * p.ldy[i] + grow] = __float2half_rn(v);
 }
 
-constexpr int kMaxScaleTiles = 32;   // row tiles whose scales a CTA stages in shared memory
 
-template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, int NWARP>
-__global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_constant__ GemvParams p) {
-  constexpr int CMAX = CLO > CHI ? CLO : CHI;
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ>
+__global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
+    qp_gemv_kernel(const __grid_constant__ GemvParams p) {
+  using PL = Plan<MODE, CLO, CHI, TB, REPS>;
+  constexpr int CMAX = PL::CMAX, NWARP = PL::NWARP, NS = PL::NS;
   uint8_t* smem = qp_smem;
   uint8_t* tab = smem;
-  if (threadIdx.x == 0 && (uint32_t)__cvta_generic_to_shared(qp_smem) != kDynSmemBase) __trap();
-  float* part = reinterpret_cast<float*>(smem + kSmemTableBytes);   // [NWARP][2][256]
+  if (threadIdx.x == 0 && smem_u32(qp_smem) != kDynSmemBase) __trap();
+  float* part = reinterpret_cast<float*>(smem + PL::TAB);   // [NWARP][2][256], aliases the rings
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  auto stamp = [&](int k) {   // debug timeline: per-warp clock64 stamps [grid][16 warps][4]
-    if (p.timeline && lane == 0 && warp < 16) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
-      p.timeline[(blockIdx.x * 16 + warp) * 8 + k] = t;
-    }
+  unsigned long long ts[8];   // debug timeline (QP_TIMELINE): clock64 stamps, stored at exit
+  auto stamp = [&](int k) {
+    if (p.timeline) asm volatile("mov.u64 %0, %%clock64;" : "=l"(ts[k]));
+  };
+  auto flush_stamps = [&](int n) {
+    if (p.timeline && lane == 0 && warp < 16)
+      for (int k = 0; k < 8; ++k) p.timeline[(blockIdx.x * 16 + warp) * 8 + k] = k < n || k >= 5 ? ts[k] : 0ull;
   };
   stamp(0);
   const int g = lane >> 2, q = lane & 3;
   // tile indices are 32-bit: the host guarantees RT*KT*gridDim < 2^32
   const uint32_t N = (uint32_t)p.RT * (uint32_t)p.KT;
-  const uint32_t T0 = N * blockIdx.x / gridDim.x, T1 = N * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t KT = p.KT;
+  // host-computed reciprocals (qp_host.cpp div_magic): no 32-bit integer divisions in the prologue
+  auto div_kt = [&](uint32_t x) -> uint32_t { return p.kt_magic ? __umulhi(x, p.kt_magic) : x / KT; };
+  auto div_grid = [&](uint32_t x) -> uint32_t { return p.grid_magic ? __umulhi(x, p.grid_magic) : x / gridDim.x; };
+  const uint32_t T0 = div_grid(N * blockIdx.x), T1 = div_grid(N * (blockIdx.x + 1));
   const uint32_t nC = T1 - T0;
   const uint32_t a = T0 + nC * warp / NWARP, b = T0 + nC * (warp + 1) / NWARP;
-  const uint32_t KT = p.KT;
   const int KH = p.KT / 2;
   const long long rowtile_bytes = (long long)KH * 512 * CLO + (long long)(KT - KH) * 512 * CHI;
 
-  auto tile_ptr = [&](uint32_t rt, int kt) -> const uint8_t* {
-    const long long off = (long long)rt * rowtile_bytes + (kt < KH ? (long long)kt * 512 * CLO
-                                                        : (long long)KH * 512 * CLO + (long long)(kt - KH) * 512 * CHI);
-    return p.codes + off;
+  // ---- this warp's code ring: NS stages, one tile each, filled by bulk async copies ----
+  const uint32_t ring = smem_u32(smem + PL::TAB) + (uint32_t)(warp * NS * PL::STAGE);
+  const uint32_t bars = smem_u32(smem + PL::BAR_OFF) + (uint32_t)(warp * NS * 8);
+  uint64_t pol = 0;
+  // issue the copy of tile t (row tile rt_, k tile kt_) into stage st (lane 0 only)
+  auto fetch = [&](uint32_t rt_, int kt_, int st, uint32_t dep = 0u) {
+    const int c = (CLO == CHI || kt_ < KH) ? CLO : CHI;
+    const long long off = (long long)rt_ * rowtile_bytes +
+                          (kt_ < KH ? (long long)kt_ * 512 * CLO : (long long)KH * 512 * CLO + (long long)(kt_ - KH) * 512 * CHI);
+    const uint32_t bar = bars + 8u * st;
+    mbar_expect_tx(bar, 512u * c);
+    bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, p.codes + off, 512u * c, bar, pol);
   };
-  auto load_tile = [&](const uint8_t* ptr, int kt, uint32_t (&buf)[4 * CMAX]) {
-    const int c = (CLO == CHI || kt < KH) ? CLO : CHI;
-    const uint4* src = reinterpret_cast<const uint4*>(ptr) + lane;
+  uint32_t rt = div_kt(a);
+  int kt = (int)(a - rt * KT);
+  if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < CMAX; ++i) {
-      if (CLO == CHI || i < c) {
-        uint4 v;
-        // streamed exactly once: no L1 allocation (no cache-policy operand: that costs two R2UR
-        // per load in the main loop)
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + i * 32));
-        buf[4 * i] = v.x; buf[4 * i + 1] = v.y; buf[4 * i + 2] = v.z; buf[4 * i + 3] = v.w;
-      }
+    for (int st = 0; st < NS; ++st) mbar_init(bars + 8u * st, 1);
+    mbar_fence_init();
+    pol = l2_evict_first_policy();
+    // only the first tile now: the whole grid's first-wave requests then complete before the
+    // second wave (issued after the table build) competes with them for HBM
+    if (a < b) fetch(rt, kt, 0);
+  }
+  // the tile NS ahead of the current one (refill target)
+  uint32_t rt_f = rt + div_kt((uint32_t)(kt + NS));
+  int kt_f = (int)((uint32_t)(kt + NS) - div_kt((uint32_t)(kt + NS)) * KT);
+
+  // per-row scales of the current row tile, rows g, g+8, g+16, g+24 (prefetched into registers
+  // when a row tile starts; consumed when its partial is flushed)
+  float sc[4];
+  auto load_scales = [&](uint32_t rt_) {
+    if constexpr (!DEQ) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sc[i] = __ldg(p.scales + rt_ * kTileRows + g + 8 * i);
     }
   };
-
-  uint32_t cur[4 * CMAX], nxt[4 * CMAX];
-  uint32_t rt = a / KT;
-  int kt = (int)(a - rt * KT);
-  const uint8_t* ptr = tile_ptr(rt, kt);
-
-  // per-row scales of this CTA's row tiles -> registers now, shared memory after the table build
-  float* sscale = reinterpret_cast<float*>(smem + kSmemTableBytes + NWARP * 2 * 256 * 4);
-  const uint32_t srt0 = T0 / KT;
-  const int n_srt = nC > 0 ? (int)((T1 - 1) / KT - srt0 + 1) : 0;
-  const bool scales_in_smem = n_srt <= kMaxScaleTiles;
-  constexpr int SC_PER_THREAD = (kMaxScaleTiles * kTileRows + NWARP * 32 - 1) / (NWARP * 32);
-  float sc_reg[SC_PER_THREAD];
-#pragma unroll
-  for (int k = 0; k < SC_PER_THREAD; ++k) {
-    const int i = tid + k * NWARP * 32;
-    sc_reg[k] = (!DEQ && scales_in_smem && i < n_srt * kTileRows) ? __ldg(p.scales + srt0 * kTileRows + i) : 0.f;
-  }
+  if (a < b) load_scales(rt);
   uint32_t xb[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) xb[i] = 0u;
   const bool xrow = !DEQ && g < p.batch;           // this lane holds a batch row of x'
   const __half* xlane = p.x + (size_t)g * p.d_in + 64 * q;
   // Everything up to griddepcontrol.wait reads only immutable layer data, so under programmatic
-  // dependent launch it may overlap the previous kernel. Order: table words (small, L2-resident),
-  // then the first tile's codes (HBM), then the table stores while the codes are in flight.
+  // dependent launch it overlaps the previous kernel: the code copies are in flight (issued
+  // above) while the table words arrive from L2 and are expanded into the replicated image.
   {
-    TableBuild<REPS, NWARP * 32> tb;
-    tb.load(p.table, p.table_words);
-    if (a < b) load_tile(ptr, kt, cur);
+    TableBuild<REPS, NWARP * 32, PL::ENTRIES> tb;
+    tb.load(p.table);
     stamp(7);
-    tb.store(p.table_words, tab);
+    tb.store(tab);
   }
   stamp(6);
+  if (lane == 0) {                                 // the rest of the ring's first fill
+    uint32_t r_ = rt;
+    int k_ = kt;
 #pragma unroll
-  for (int k = 0; k < SC_PER_THREAD; ++k) {
-    const int i = tid + k * NWARP * 32;
-    if (!DEQ && scales_in_smem && i < n_srt * kTileRows) sscale[i] = sc_reg[k];
+    for (int st = 1; st < NS; ++st) {
+      if (++k_ == (int)KT) { k_ = 0; ++r_; }
+      if (a + st < b) fetch(r_, k_, st);
+    }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   stamp(5);
@@ -319,23 +401,42 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
     load_x8(xb + 8, xlane + kt * kTileCols + 16);
   }
   __syncthreads();
-  auto scale_of = [&](uint32_t rt_, int row) -> float {
-    return scales_in_smem ? sscale[(rt_ - srt0) * kTileRows + row] : __ldg(p.scales + rt_ * kTileRows + row);
-  };
+  auto scale_of = [&](uint32_t rt_, int row) -> float { return __ldg(p.scales + rt_ * kTileRows + row); };
 
   stamp(1);
   const uint32_t laneoff = (uint32_t)(lane % REPS) * 4u;
   float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-  const uint32_t a_rt = a / KT;
+  const uint32_t a_rt = rt;
 
-  // One tile: prefetch the next tile's stream into `nb`, decode `cb`. (Ping-ponging the two
-  // buffers instead of copying doubles the code size and measured no faster on B200.)
-  auto process = [&](uint32_t t, uint32_t (&cb)[4 * CMAX], uint32_t (&nb)[4 * CMAX]) {
+  float hp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};   // head / tail row-tile partials
+  float tp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  uint32_t cur[4 * CMAX];
+  int st = 0;
+  uint32_t par = 0;
+  for (uint32_t t = a; t < b; ++t) {
+    // ---- this tile's stream words: stage st -> registers (c conflict-free 128-bit loads) ----
+    mbar_wait(bars + 8u * st, par);
+    {
+      const int c = (CLO == CHI || kt < KH) ? CLO : CHI;
+      const uint32_t src = ring + (uint32_t)(st * PL::STAGE) + (uint32_t)lane * 16u;
+#pragma unroll
+      for (int i = 0; i < CMAX; ++i) {
+        if (CLO == CHI || i < c) {
+          const uint4 v = lds128(src + i * 512);
+          cur[4 * i] = v.x; cur[4 * i + 1] = v.y; cur[4 * i + 2] = v.z; cur[4 * i + 3] = v.w;
+        }
+      }
+      // The stage is free once every lane's shared loads have returned: a warp reduction over the
+      // last loaded word of each lane (in-order shared pipeline: the earlier loads are done too)
+      // makes lane 0's refill depend on all of them (p.zero == 0 keeps the value unchanged).
+      const uint32_t last = (CLO == CHI || c == CMAX) ? cur[4 * CMAX - 1] : cur[4 * CLO - 1];
+      const uint32_t dep = __reduce_or_sync(0xffffffffu, last & p.zero);
+      if (lane == 0 && t + NS < b) fetch(rt_f, kt_f, st, dep);
+      if (++kt_f == (int)KT) { kt_f = 0; ++rt_f; }
+    }
     int kt_n = kt + 1;
     uint32_t rt_n = rt;
     if (kt_n == (int)KT) { kt_n = 0; ++rt_n; }
-    const uint8_t* ptr_n = (CLO == CHI) ? ptr + 512 * CLO : tile_ptr(rt_n, kt_n);
-    if (t + 1 < b) load_tile(ptr_n, kt_n, nb);
     const __half* x_hi = xrow ? xlane + kt * kTileCols + 32 : nullptr;
     const __half* x_next = (xrow && t + 1 < b) ? xlane + kt_n * kTileCols : nullptr;
     uint32_t* wout_lane = nullptr;
@@ -345,9 +446,10 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
       wout_lane = reinterpret_cast<uint32_t*>(p.w_out) + (size_t)(rt * kTileRows + g) * ldw + (kt * kTileCols + 64 * q) / 2;
     }
     if (CLO == CHI || kt < KH)
-      tile_body<MODE, CLO, L, TB, REPS, DEQ>(cb, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next);
+      tile_body<MODE, CLO, L, TB, REPS, DEQ>(cur, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next);
     else
-      tile_body<MODE, CHI, L, TB, REPS, DEQ>(cb, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next);
+      tile_body<MODE, CHI, L, TB, REPS, DEQ>(cur, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next);
+    if (++st == NS) { st = 0; par ^= 1u; }
 
     if constexpr (!DEQ) {
       if (kt == (int)KT - 1 || t == b - 1) {
@@ -359,7 +461,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-              if (bb < p.batch) store_out(p, (int)rt, row, bb, acc[m][r], scale_of(rt, row));
+              if (bb < p.batch) store_out(p, (int)rt, row, bb, acc[m][r], sc[2 * m + (r >> 1)]);
             }
         } else if (p.y_atomic) {
           // y was zeroed by the preceding kernel: add this warp's scaled partial straight into it
@@ -373,47 +475,46 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-              if (bb < p.batch) atomicAdd(yb + (size_t)bb * p.ldy[i] + row, acc[m][r] * scale_of(rt, row));
+              if (bb < p.batch) atomicAdd(yb + (size_t)bb * p.ldy[i] + row, acc[m][r] * sc[2 * m + (r >> 1)]);
             }
         } else {
-          float* slot = part + (warp * 2 + (rt == a_rt ? 0 : 1)) * 256;
+          // partial of a row tile shared with other warps / CTAs: kept in registers until every
+          // warp has left the main loop (the partial slots alias the code rings)
+          const bool head = rt == a_rt;
 #pragma unroll
           for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-              slot[row * 8 + bb] = acc[m][r];
-            }
+            for (int r = 0; r < 4; ++r) (head ? hp : tp)[m][r] = acc[m][r];
         }
 #pragma unroll
         for (int m = 0; m < 2; ++m)
 #pragma unroll
           for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
+        if (t + 1 < b) load_scales(rt_n);
       }
     }
-    kt = kt_n; rt = rt_n; ptr = ptr_n;
-  };
-#ifdef QP_PINGPONG
-  // two tiles per iteration with the buffers' roles swapped: no register copies
-  uint32_t t = a;
-  for (; t + 1 < b; t += 2) {
-    process(t, cur, nxt);
-    process(t + 1, nxt, cur);
+    kt = kt_n; rt = rt_n;
   }
-  if (t < b) process(t, cur, nxt);
-#else
-  for (uint32_t t = a; t < b; ++t) {
-    process(t, cur, nxt);
-#pragma unroll
-    for (int i = 0; i < 4 * CMAX; ++i) cur[i] = nxt[i];
-  }
-#endif
   stamp(2);
   asm volatile("griddepcontrol.launch_dependents;");
-  if constexpr (DEQ) return;
-  if (nC <= 0 || p.y_atomic) return;
+  if (DEQ || nC <= 0 || p.y_atomic) {
+    flush_stamps(3);
+    return;
+  }
 
   // ---- reduction of the warp partials: one warp per row tile, no CTA-wide barrier in the loop ----
+  __syncthreads();                                    // every warp is done with its code ring
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float* slot = part + (warp * 2 + h) * 256;
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
+        slot[row * 8 + bb] = h == 0 ? hp[m][r] : tp[m][r];
+      }
+  }
   __syncthreads();
   stamp(4);
   // lane w < NWARP holds warp w's tile range (no divisions inside the loops below)
@@ -509,42 +610,33 @@ __global__ void __launch_bounds__(NWARP * 32, 1) qp_gemv_kernel(const __grid_con
   }
   __syncthreads();
   stamp(3);
+  flush_stamps(8);
 }
 
-template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, int NW>
-cudaError_t launch_nw(const GemvParams& prm, int grid, bool pdl, cudaStream_t s) {
-  const int smem = kSmemTableBytes + NW * 2 * 256 * 4 + kMaxScaleTiles * kTileRows * 4;
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ>
+cudaError_t launch_plan(const GemvParams& prm, int grid, bool pdl, cudaStream_t s) {
+  using PL = Plan<MODE, CLO, CHI, TB, REPS>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NW * 32);
-  cfg.dynamicSmemBytes = smem;
+  cfg.blockDim = dim3(PL::NWARP * 32);
+  cfg.dynamicSmemBytes = PL::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, DEQ, NW>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, DEQ>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM);
   if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k, prm);
   return e;
 }
 
-int tune_nwarp();   // QP_NWARP environment override (tuning experiments), 0 = default
-
-template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool TUNE = false>
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool UNUSED = false>
 struct GemvVariant {
-  static constexpr int CMAX = CLO > CHI ? CLO : CHI;
-  static constexpr int NWARP = CMAX <= 6 ? 16 : 12;   // register budget
   static cudaError_t launch(const GemvParams& prm, int grid, int /*nwarps*/, bool dequant, bool pdl, cudaStream_t s) {
-    if (dequant) return launch_nw<MODE, CLO, CHI, L, TB, REPS, true, NWARP>(prm, grid, pdl, s);
-    if constexpr (TUNE) {
-      const int nw = tune_nwarp();
-      if (nw == 8) return launch_nw<MODE, CLO, CHI, L, TB, REPS, false, 8>(prm, grid, pdl, s);
-      if (nw == 12) return launch_nw<MODE, CLO, CHI, L, TB, REPS, false, 12>(prm, grid, pdl, s);
-      if (nw == 16 && CMAX <= 8) return launch_nw<MODE, CLO, CHI, L, TB, REPS, false, (CMAX <= 8 ? 16 : 12)>(prm, grid, pdl, s);
-    }
-    return launch_nw<MODE, CLO, CHI, L, TB, REPS, false, NWARP>(prm, grid, pdl, s);
+    if (dequant) return launch_plan<MODE, CLO, CHI, L, TB, REPS, true>(prm, grid, pdl, s);
+    return launch_plan<MODE, CLO, CHI, L, TB, REPS, false>(prm, grid, pdl, s);
   }
   static void reg() { register_gemv(KernelKey{MODE, CLO, CHI, L, TB, REPS}, &launch); }
 };

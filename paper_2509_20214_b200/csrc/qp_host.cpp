@@ -197,6 +197,10 @@ qp_status make_kernel_key(const qp_codebook* cb, qp_scheme scheme, int c_lo, int
     if (cb->mode == DEC_LUT2) *k = KernelKey{DEC_LUT2, c_lo, c_lo, 0, 0, cb->reps};
     else *k = KernelKey{DEC_SCALAR, c_lo, c_lo, 0, cb->tb, cb->reps};
   }
+  // the kernels expand exactly this many compact-table words (TableBuild, no bounds checks)
+  const int entries = k->mode == DEC_TCQ_PRESIGNED ? (2 << k->tb) : k->mode == DEC_LUT2 ? (1 << k->c_lo) : (1 << k->tb);
+  if (cb->table_words != entries)
+    return fail(QP_ERR_CONFIG_MISMATCH, "codebook table has %d words, the decoder expects %d", cb->table_words, entries);
   return QP_OK;
 }
 
@@ -254,7 +258,7 @@ qp_status layer_init(qp_layer* l, int d_out, int d_in, qp_scheme scheme, int bit
   l->code_bytes = layout_bytes(scheme, bits_x4, d_out, d_in);
   l->cb = cb;
   l->rht = r;
-  make_kernel_key(cb, scheme, l->c_lo, l->c_hi, &l->key);
+  if (qp_status st = make_kernel_key(cb, scheme, l->c_lo, l->c_hi, &l->key); st != QP_OK) return st;
   l->launcher = find_gemv(l->key);
   if (!l->launcher)
     return fail(QP_ERR_UNSUPPORTED, "no compiled kernel variant for mode=%d c=%d/%d L=%d tb=%d reps=%d. Remedy: add it "
@@ -306,6 +310,19 @@ qp_status run_rht(const qp_rht* r, const void* x, qp_dtype xt, int batch, __half
   return QP_OK;
 }
 
+// ceil(2^32 / d) when floor(x / d) == __umulhi(x, m) for every x <= x_max (x * (m*d - 2^32) < 2^32
+// suffices since m*d - 2^32 < d), else 0 (the kernel then divides).
+uint32_t div_magic(uint64_t d, uint64_t x_max) {
+  if (d <= 1 || x_max * d >= (1ull << 32)) return 0;
+  return (uint32_t)(((1ull << 32) + d - 1) / d);
+}
+
+void set_magics(GemvParams& p, int grid) {
+  const uint64_t N = (uint64_t)p.RT * (uint64_t)p.KT;
+  p.kt_magic = div_magic((uint64_t)p.KT, N + 8);
+  p.grid_magic = div_magic((uint64_t)grid, N * (uint64_t)grid);
+}
+
 // CTAs of the zeroing kernel: one per 64 KB of fp32 output, 1..8
 int zero_ctas(const long long* zn, int n) {
   long long bytes = 0;
@@ -344,6 +361,7 @@ qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, co
   p.timeline = tl ? d_tl : nullptr;
   int grid = l->grid;
   if (pdl && side_ctas > 0 && side_ctas <= kMaxSideCtas) grid = std::max(1, std::min(grid, num_sms() - side_ctas));
+  set_magics(p, grid);
   cudaError_t e = l->launcher(p, grid, 0, false, pdl, s);
   if (e != cudaSuccess) return cuda_fail(e, "fused dequant-GEMV launch");
   count_launch();
@@ -389,6 +407,10 @@ qp_status check_fwd_args(const void* x, qp_dtype xt, int batch, qp_dtype yt, uns
 }
 
 }  // namespace
+
+namespace qp {
+int set_error(int status, const char* msg) { return (int)fail((qp_status)status, "%s", msg); }
+}  // namespace qp
 
 // ---------------------------------------------------------------------------------------
 // C ABI
@@ -651,6 +673,7 @@ qp_status qp_dequantize(const qp_layer* l, void* W_hat_fp16, void* stream) {
   p.d_in = l->d_in;
   p.batch = 1;
   p.w_out = static_cast<__half*>(W_hat_fp16);
+  set_magics(p, l->grid);
   cudaError_t e = l->launcher(p, l->grid, 0, true, false, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "dequantize launch");
   count_launch();

@@ -42,6 +42,8 @@ struct GemvParams {
   const uint32_t* table;       // compact device table (table_words uint32 = half2)
   int table_words;
   int RT, KT;                  // row tiles, k tiles
+  // x / KT and x / gridDim.x as __umulhi(x, magic) (exact for the x that occur; 0 = divide)
+  uint32_t kt_magic, grid_magic;
   int d_in;
   int batch;                   // 1..8
   const __half* x;             // R x, [batch][d_in] fp16
@@ -52,6 +54,7 @@ struct GemvParams {
   int ldy[kMaxGroup];          // leading dimension (elements) of y[i] rows (= d_out_i)
   int y_f32;                   // 1: fp32 output, 0: fp16 output
   int y_atomic;                // 1: y was zeroed; CTAs sharing a row tile red.add their scaled partials
+  uint32_t zero;               // always 0 (an operand the compiler cannot constant-fold)
   // cross-CTA fixup workspace
   float* ws;                   // [grid][256] cross-CTA partials (slot = contributing CTA)
   int* counters;               // [RT], zero between launches (self-resetting)
@@ -86,5 +89,6 @@ cudaError_t launch_zero(const RhtParams& p, int grid, bool pdl, cudaStream_t s);
 cudaError_t launch_gather_permute(const void* src, void* dst, int world, int batch, int m, int elem_bytes,
                                   cudaStream_t s);
 void count_launch();
+int set_error(int status, const char* msg);   // qp_last_error() message of the calling thread
 
 }  // namespace qp

@@ -1,0 +1,136 @@
+"""BASELINE.json configs[4] ("C5"): one Llama-3.1-8B decoder layer with a mixed-scheme
+assignment, fused QKV and up-gate groups, batch 1 and 8, on one B200.
+
+    python tools/decoder_layer.py [--batches 1,8] [--steps 50] [--out gpurun_out/c5.jsonl]
+
+Bit allocation: Theorem 1 through the library's host-only qp_optimal_bits, with
+synthetic sensitivities a_l = 1 (the paper's a_l need a model and data: out of
+scope), eta = 1.5 and a budget of 3.25 bits/weight on average over the 7 matrices. That gives
+q/o 3.94, k/v 4.94, MLP 3.04 bits. Palette assignment:
+  * QKV: one quantizer for the fused group, its size-weighted allocation 4.27 rounded
+    to the palette's 0.25-bit grid -> half-TCQ 4.25 (TCQ-4.0 | TCQ-4.5 halves, tlut 10 bits);
+  * o (3.94): NUQ-4;   up / gate (3.04): TCQ-3.0 (fused group);   down (3.04): VQ-3.0.
+One step = the 4 ops of a decoder layer, each = rotation of its input + fused dequant-GEMV
+(qp_fused_linear / qp_linear_fwd), in one CUDA graph; R replicas of the layer (> 2x L2) cycle.
+The ops use independent synthetic inputs (no attention / activation function between them: the
+path measured is the quantized linear layers).
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2509_20214_b200 import _lib as QL  # noqa: E402
+from qp_synth import activations_fp16, channel_scales, random_code_bytes  # noqa: E402
+from tools import palette as P  # noqa: E402
+
+H, KV, FF = 4096, 1024, 14336
+MATS = [("q", H, H), ("k", KV, H), ("v", KV, H), ("o", H, H), ("gate", FF, H), ("up", FF, H), ("down", H, FF)]
+
+
+def allocation():
+    n = np.array([o * i for _, o, i in MATS], dtype=float)
+    b = QL.optimal_bits(np.ones(len(MATS)), n, 3.25 * n.sum(), 1.5)
+    qkv = float((b[:3] * n[:3]).sum() / n[:3].sum())
+    return {m[0]: round(float(x), 4) for m, x in zip(MATS, b)}, round(qkv, 4)
+
+
+OPS = [  # (op, member matrices, scheme, bits_x4)
+    ("qkv", ["q", "k", "v"], "half_tcq", 17),
+    ("o", ["o"], "nuq", 16),
+    ("gate_up", ["gate", "up"], "tcq", 12),
+    ("down", ["down"], "vq", 12),
+]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batches", default="1,8")
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "c5.jsonl"))
+    a = ap.parse_args()
+    bits, qkv_bits = allocation()
+    shapes = {m: (o, i) for m, o, i in MATS}
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    cbs, rots = {}, {}
+    layer_bytes = sum(P.code_bytes(*shapes[m], s, x4) for _, ms, s, x4 in OPS for m in ms)
+    R = max(2, -(-2 * l2 // layer_bytes) + 1)
+    reps = []
+    for r in range(R):
+        ops = []
+        for name, members, scheme, x4 in OPS:
+            key = (scheme, x4)
+            if key not in cbs:
+                cbs[key] = QL.Codebook(scheme, x4, P.load_fp16(scheme, x4), L=16)
+            d_in = shapes[members[0]][1]
+            if d_in not in rots:
+                rots[d_in] = QL.Rht(7, d_in)
+            lays = []
+            for j, m in enumerate(members):
+                d_out = shapes[m][0]
+                codes = random_code_bytes(P.code_bytes(d_out, d_in, scheme, x4), 1000 + 10 * r + j)
+                lays.append(QL.Layer.from_codes(codes, channel_scales(d_out, d_in), d_out, d_in, scheme, x4,
+                                                cbs[key], rots[d_in]))
+            ops.append((members, QL.Group(lays) if len(lays) > 1 else lays[0], lays, d_in))
+        reps.append(ops)
+    peak = 6535.1
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peak = float(json.load(open(pk))["hbm_gbs"])
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    for batch in [int(b) for b in a.batches.split(",")]:
+        xs = {d: torch.from_numpy(activations_fp16(batch, d)).cuda() for d in (H, FF)}
+        ys = {m: torch.empty(batch, shapes[m][0], device="cuda") for m, _, _ in MATS}
+        alg = 0
+        for name, members, scheme, x4 in OPS:
+            d_in = shapes[members[0]][1]
+            for m in members:
+                d_out = shapes[m][0]
+                alg += P.code_bytes(d_out, d_in, scheme, x4) + 4 * d_out + 4 * batch * d_out
+            alg += P.lut_bytes(scheme, x4) + 2 * batch * d_in + 4 * batch * d_in   # x' in + rotation
+        st = torch.cuda.Stream()
+
+        def step(ops):
+            for members, op, lays, d_in in ops:
+                if isinstance(op, QL.Group):
+                    op.forward(xs[d_in], batch, [ys[m] for m in members], stream=st)
+                else:
+                    op.forward(xs[d_in], batch, ys[members[0]], stream=st)
+
+        n0 = QL.launch_count()
+        with torch.cuda.stream(st):
+            for r in range(R):
+                step(reps[r])
+            st.synchronize()
+            launches = (QL.launch_count() - n0) // R
+            K = max(a.steps // R, 1) * R
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                for k in range(K):
+                    step(reps[k % R])
+            for _ in range(3):
+                g.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(5):
+                g.replay()
+            e1.record(st)
+            e1.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / (5 * K)
+        line = {"config": "C5: Llama-3.1-8B decoder layer, mixed schemes, fused QKV / up-gate", "batch": batch,
+                "us_per_decoder_layer": round(us, 3), "alg_bytes": alg, "gbs": round(alg / us / 1e3, 1),
+                "frac_of_hbm_peak": round(alg / us / 1e3 / peak, 4), "peak_gbs": peak, "kernels_per_layer": launches,
+                "replicas": R, "allocation_bits": bits, "qkv_group_bits": qkv_bits,
+                "assignment": {o[0]: f"{o[2]}-{o[3] / 4}" for o in OPS}}
+        print(json.dumps(line), flush=True)
+        with open(a.out, "a") as f:
+            f.write(json.dumps(line) + "\n")
+
+
+if __name__ == "__main__":
+    main()
