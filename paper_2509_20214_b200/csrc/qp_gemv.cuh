@@ -24,6 +24,7 @@
 //    griddepcontrol.wait (they read only immutable layer data).
 #pragma once
 #include <cuda_fp16.h>
+#include <algorithm>
 #include <utility>
 
 #include "qp_internal.h"
@@ -186,12 +187,28 @@ __device__ __forceinline__ void load_x8(uint32_t* dst, const __half* src) {   //
 // tile's activations (x_hi) is loaded when the tile starts and the first half of the next tile's
 // (x_next) once kappa 0..7 are done, so activation loads never sit on the critical path and
 // need no extra registers. Lanes with no batch row (x_hi == nullptr) keep zeros.
-template <int MODE, int C, int L, int TB, int REPS, bool DEQ>
-__device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, uint32_t* xb, float (&acc)[2][4],
+#ifdef QP_ACC4
+constexpr int kAccSets = 2;   // independent accumulator chains per row block (k-step parity)
+#else
+constexpr int kAccSets = 1;
+#endif
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+
+template <int MODE, int C, int L, int TB, int REPS, bool DEQ, bool XS>
+__device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, uint32_t* xb, float (&acc)[2 * kAccSets][4],
                                           uint32_t* wout_lane, int ldw_words, const __half* x_hi,
-                                          const __half* x_next) {
+                                          const __half* x_next, uint32_t xs_addr) {
   using D = Dec<MODE, C, L, TB, REPS>;
-  if constexpr (!DEQ) {
+  if constexpr (!DEQ && XS) {
+    const uint2 bx = lds64(xs_addr);
+    xb[0] = bx.x;
+    xb[1] = bx.y;
+  }
+  if constexpr (!DEQ && !XS) {
     if (x_hi) {
       load_x8(xb + 16, x_hi);
       load_x8(xb + 24, x_hi + 16);
@@ -213,11 +230,19 @@ __device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, u
         p[8 * ldw_words] = a1;
         p[1] = a2;
         p[8 * ldw_words + 1] = a3;
+      } else if constexpr (XS) {
+        // B fragment of k-step kap in xb[2(kap&1)..]; the next one is requested one k-step ahead
+        if constexpr (m == 0 && kap + 1 < 16) {
+          const uint2 bx = lds64(xs_addr + 8 * (kap + 1));
+          xb[2 * ((kap + 1) & 1)] = bx.x;
+          xb[2 * ((kap + 1) & 1) + 1] = bx.y;
+        }
+        mma16816(acc[m + 2 * (kap % kAccSets)], a0, a1, a2, a3, xb[2 * (kap & 1)], xb[2 * (kap & 1) + 1]);
       } else {
-        mma16816(acc[m], a0, a1, a2, a3, xb[2 * kap], xb[2 * kap + 1]);
+        mma16816(acc[m + 2 * (kap % kAccSets)], a0, a1, a2, a3, xb[2 * kap], xb[2 * kap + 1]);
       }
     });
-    if constexpr (!DEQ && kap == 7) {
+    if constexpr (!DEQ && !XS && kap == 7) {
       if (x_next) {
         load_x8(xb, x_next);
         load_x8(xb + 8, x_next + 16);
@@ -256,32 +281,42 @@ struct TableBuild {
   }
 };
 
-// Compile-time shared-memory plan of one kernel variant:
+// Shared-memory plan of one kernel variant (compile-time part):
 //   [0, TAB)                     replicated decode table (entries x REPS x 4 B)
-//   [TAB, TAB + RING)            per-warp code rings: NWARP x NS stages x 512*CMAX bytes
-//                                (aliased by the epilogue's warp partials, used after the loop)
-//   [.., + 8*NWARP*NS)           one mbarrier per stage
-template <int MODE, int CLO, int CHI, int TB, int REPS>
+//   [TAB, TAB + 1024)            one mbarrier per ring stage (<= 16 warps x 4 stages)
+//   [XS_OFF, + xs_bytes)         x' of every batch row, padded layout (XS variants only)
+//   [.., + NWARP * ns * STAGE)   per-warp code rings of ns stages, 512*CMAX bytes each
+// The epilogue's warp partials alias [XS_OFF, ...) after the loop. ns and xs_bytes are chosen at
+// launch (launch_plan) from the batch and d_in.
+#ifndef QP_XS_WARPS
+#define QP_XS_WARPS 16
+#endif
+template <int MODE, int CLO, int CHI, int TB, int REPS, bool XS = false>
 struct Plan {
   static constexpr int CMAX = CLO > CHI ? CLO : CHI;
   static constexpr int ENTRIES = MODE == DEC_TCQ_PRESIGNED ? (2 << TB) : MODE == DEC_LUT2 ? (1 << CLO) : (1 << TB);
   static constexpr int TAB = ENTRIES * REPS * 4 < 4096 ? 4096 : ENTRIES * REPS * 4;
   static constexpr int SMEM_MAX = 232448;          // sm_100 opt-in per block
   static constexpr int STAGE = 512 * CMAX;
-  static constexpr int NW0 = CMAX <= 8 ? 16 : 12;  // register budget (128 regs x 512 threads)
-  static constexpr int ns_for(int nw) {
-    const int n = (SMEM_MAX - TAB - 1024) / (nw * STAGE);
-    return n > 4 ? 4 : n;
-  }
-  static constexpr int NWARP = ns_for(NW0) >= 1 ? NW0 : (ns_for(12) >= 1 ? 12 : 8);
-  static constexpr int NS = ns_for(NWARP);   // a stage is refilled as soon as it is read: NS tiles ahead
+  // register budget (128 regs x 512 threads, no spills); x' in shared memory frees the 32
+  // B-fragment registers (QP_XS_WARPS experiments with more warps)
+  static constexpr int NWARP = CMAX <= 6 ? (XS ? QP_XS_WARPS : 16) : 12;
+  static constexpr int BAR_OFF = TAB;
+  static constexpr int XS_OFF = TAB + 1024;
   static constexpr int PART = NWARP * 2 * 256 * 4;  // epilogue warp partials
-  static constexpr int RING = NWARP * NS * STAGE > PART ? NWARP * NS * STAGE : PART;
-  static constexpr int BAR_OFF = TAB + RING;
-  static constexpr int SMEM = BAR_OFF + ((8 * NWARP * NS + 127) / 128) * 128;
-  static_assert(NS >= 1 && SMEM <= SMEM_MAX, "shared-memory plan does not fit");
+  static constexpr int AVAIL = SMEM_MAX - XS_OFF;   // for x' + rings
+  static_assert(AVAIL >= NWARP * STAGE && AVAIL >= PART, "shared-memory plan does not fit");
 };
 
+// x' staged in shared memory (XS): batch row g at g*RS, element k at (k/64)*136 + (k%64)*2 within
+// the row, RS = 136*(d_in/64) rounded up to 32 (mod 128). A lane's B fragment for k-step kappa
+// (4 consecutive elements 64q + 4kappa, LAYOUT.md section 2) is one 8-byte load; the 8-byte pad
+// per 64-element group and RS = 32 (mod 128) put the 16 lanes of a half-warp (g < 4, q < 4) on
+// 16 distinct bank pairs: conflict-free.
+__host__ __device__ constexpr int xs_row_stride(int d_in) {
+  const int base = (d_in / 64) * 136;
+  return base + ((32 - base % 128) + 128) % 128;
+}
 
 __device__ __forceinline__ uint32_t owner_of(uint32_t t, uint32_t lo, uint32_t n, uint32_t parts) {
   // part p owns [lo + n*p/parts, lo + n*(p+1)/parts); returns the p that contains t
@@ -299,18 +334,20 @@ __device__ __forceinline__ void store_out(const GemvParams& p, int rt, int row, 
 }
 
 
-template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ>
-__global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, bool XS>
+__global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32, 1)
     qp_gemv_kernel(const __grid_constant__ GemvParams p) {
-  using PL = Plan<MODE, CLO, CHI, TB, REPS>;
-  constexpr int CMAX = PL::CMAX, NWARP = PL::NWARP, NS = PL::NS;
+  using PL = Plan<MODE, CLO, CHI, TB, REPS, XS>;
+  constexpr int CMAX = PL::CMAX, NWARP = PL::NWARP;
+  const int NS = p.ns;
   uint8_t* smem = qp_smem;
   uint8_t* tab = smem;
   if (threadIdx.x == 0 && smem_u32(qp_smem) != kDynSmemBase) __trap();
-  float* part = reinterpret_cast<float*>(smem + PL::TAB);   // [NWARP][2][256], aliases the rings
+  float* part = reinterpret_cast<float*>(smem + PL::XS_OFF);   // [NWARP][2][256], aliases x' + rings
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  unsigned long long ts[8];   // debug timeline (QP_TIMELINE): clock64 stamps, stored at exit
+#ifdef QP_KERNEL_TIMELINE
+  unsigned long long ts[8];   // debug timeline (build with -DQP_KERNEL_TIMELINE, run with QP_TIMELINE=1)
   auto stamp = [&](int k) {
     if (p.timeline) asm volatile("mov.u64 %0, %%clock64;" : "=l"(ts[k]));
   };
@@ -318,6 +355,10 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
     if (p.timeline && lane == 0 && warp < 16)
       for (int k = 0; k < 8; ++k) p.timeline[(blockIdx.x * 16 + warp) * 8 + k] = k < n || k >= 5 ? ts[k] : 0ull;
   };
+#else
+  auto stamp = [](int) {};
+  auto flush_stamps = [](int) {};
+#endif
   stamp(0);
   const int g = lane >> 2, q = lane & 3;
   // tile indices are 32-bit: the host guarantees RT*KT*gridDim < 2^32
@@ -333,7 +374,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
   const long long rowtile_bytes = (long long)KH * 512 * CLO + (long long)(KT - KH) * 512 * CHI;
 
   // ---- this warp's code ring: NS stages, one tile each, filled by bulk async copies ----
-  const uint32_t ring = smem_u32(smem + PL::TAB) + (uint32_t)(warp * NS * PL::STAGE);
+  const uint32_t ring = smem_u32(smem + PL::XS_OFF + p.xs_bytes) + (uint32_t)(warp * NS * PL::STAGE);
   const uint32_t bars = smem_u32(smem + PL::BAR_OFF) + (uint32_t)(warp * NS * 8);
   uint64_t pol = 0;
   // issue the copy of tile t (row tile rt_, k tile kt_) into stage st (lane 0 only)
@@ -370,9 +411,10 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
     }
   };
   if (a < b) load_scales(rt);
-  uint32_t xb[32];
+  constexpr int NXB = XS ? 4 : 32;                 // B-fragment registers
+  uint32_t xb[NXB];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) xb[i] = 0u;
+  for (int i = 0; i < NXB; ++i) xb[i] = 0u;
   const bool xrow = !DEQ && g < p.batch;           // this lane holds a batch row of x'
   const __half* xlane = p.x + (size_t)g * p.d_in + 64 * q;
   // Everything up to griddepcontrol.wait reads only immutable layer data, so under programmatic
@@ -396,7 +438,18 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   stamp(5);
-  if (xrow && a < b) {                             // first tile, kappa 0..7
+  // this lane's x' row in the staged copy (lanes without a batch row read row batch-1: their
+  // products land in y columns that are never stored)
+  const uint32_t xs_lane = smem_u32(smem + PL::XS_OFF) + (uint32_t)(min(g, p.batch - 1) * p.xs_rs + q * 136);
+  if constexpr (XS) {
+    // x' (the previous kernel's output) -> padded shared layout, 8 bytes per thread-step
+    const int units = p.d_in / 4;                  // 8-byte units per row
+    for (int i = tid; i < p.batch * units; i += NWARP * 32) {
+      const int row = i / units, k = (i - row * units) * 4;
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(p.x + (size_t)row * p.d_in + k));
+      *reinterpret_cast<uint2*>(smem + PL::XS_OFF + row * p.xs_rs + (k >> 6) * 136 + (k & 63) * 2) = v;
+    }
+  } else if (xrow && a < b) {                      // first tile, kappa 0..7
     load_x8(xb, xlane + kt * kTileCols);
     load_x8(xb + 8, xlane + kt * kTileCols + 16);
   }
@@ -405,11 +458,14 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
 
   stamp(1);
   const uint32_t laneoff = (uint32_t)(lane % REPS) * 4u;
-  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  float acc[2 * kAccSets][4];
+#pragma unroll
+  for (int m = 0; m < 2 * kAccSets; ++m)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
   const uint32_t a_rt = rt;
 
-  float hp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};   // head / tail row-tile partials
-  float tp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+  float hp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};   // head row-tile partial
   uint32_t cur[4 * CMAX];
   int st = 0;
   uint32_t par = 0;
@@ -437,22 +493,29 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
     int kt_n = kt + 1;
     uint32_t rt_n = rt;
     if (kt_n == (int)KT) { kt_n = 0; ++rt_n; }
-    const __half* x_hi = xrow ? xlane + kt * kTileCols + 32 : nullptr;
-    const __half* x_next = (xrow && t + 1 < b) ? xlane + kt_n * kTileCols : nullptr;
+    const __half* x_hi = (!XS && xrow) ? xlane + kt * kTileCols + 32 : nullptr;
+    const __half* x_next = (!XS && xrow && t + 1 < b) ? xlane + kt_n * kTileCols : nullptr;
     uint32_t* wout_lane = nullptr;
     int ldw = 0;
     if constexpr (DEQ) {
       ldw = p.d_in / 2;
       wout_lane = reinterpret_cast<uint32_t*>(p.w_out) + (size_t)(rt * kTileRows + g) * ldw + (kt * kTileCols + 64 * q) / 2;
     }
+    const uint32_t xs_addr = xs_lane + (uint32_t)(kt * 4 * 136);
     if (CLO == CHI || kt < KH)
-      tile_body<MODE, CLO, L, TB, REPS, DEQ>(cur, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next);
+      tile_body<MODE, CLO, L, TB, REPS, DEQ, XS>(cur, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next, xs_addr);
     else
-      tile_body<MODE, CHI, L, TB, REPS, DEQ>(cur, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next);
+      tile_body<MODE, CHI, L, TB, REPS, DEQ, XS>(cur, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next, xs_addr);
     if (++st == NS) { st = 0; par ^= 1u; }
 
     if constexpr (!DEQ) {
       if (kt == (int)KT - 1 || t == b - 1) {
+        if constexpr (kAccSets == 2) {
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) { acc[m][r] += acc[m + 2][r]; acc[m + 2][r] = 0.f; }
+        }
         const uint32_t rs = rt * KT;
         const bool own = (a <= rs) && (b >= rs + KT);
         if (own) {
@@ -477,19 +540,22 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
               const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
               if (bb < p.batch) atomicAdd(yb + (size_t)bb * p.ldy[i] + row, acc[m][r] * sc[2 * m + (r >> 1)]);
             }
-        } else {
-          // partial of a row tile shared with other warps / CTAs: kept in registers until every
-          // warp has left the main loop (the partial slots alias the code rings)
-          const bool head = rt == a_rt;
+        } else if (t + 1 < b) {
+          // partial of a row tile shared with other warps / CTAs, kept in registers until every
+          // warp has left the main loop (the partial slots alias x' and the code rings). Only the
+          // head row tile can end before the range does (middle row tiles are owned); the tail
+          // partial simply stays in acc.
 #pragma unroll
           for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) (head ? hp : tp)[m][r] = acc[m][r];
+            for (int r = 0; r < 4; ++r) hp[m][r] = acc[m][r];
         }
+        if (own || p.y_atomic || t + 1 < b) {
 #pragma unroll
-        for (int m = 0; m < 2; ++m)
+          for (int m = 0; m < 2; ++m)
 #pragma unroll
-          for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
+            for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
+        }
         if (t + 1 < b) load_scales(rt_n);
       }
     }
@@ -504,6 +570,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
 
   // ---- reduction of the warp partials: one warp per row tile, no CTA-wide barrier in the loop ----
   __syncthreads();                                    // every warp is done with its code ring
+  const bool single_rt = a >= b || div_kt(b - 1) == a_rt;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     float* slot = part + (warp * 2 + h) * 256;
@@ -512,7 +579,8 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-        slot[row * 8 + bb] = h == 0 ? hp[m][r] : tp[m][r];
+        // one row tile only: its partial is in acc (slot 0); else head in hp, tail in acc
+        slot[row * 8 + bb] = h == 0 ? (single_rt ? acc[m][r] : hp[m][r]) : (single_rt ? 0.f : acc[m][r]);
       }
   }
   __syncthreads();
@@ -613,23 +681,46 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS>::NWARP * 32, 1)
   flush_stamps(8);
 }
 
-template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ>
-cudaError_t launch_plan(const GemvParams& prm, int grid, bool pdl, cudaStream_t s) {
-  using PL = Plan<MODE, CLO, CHI, TB, REPS>;
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, bool XS>
+cudaError_t launch_one(const GemvParams& prm, int grid, bool pdl, cudaStream_t s) {
+  using PL = Plan<MODE, CLO, CHI, TB, REPS, XS>;
+  const int smem = PL::XS_OFF + (std::max)(prm.xs_bytes + PL::NWARP * prm.ns * PL::STAGE, PL::PART);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(PL::NWARP * 32);
-  cfg.dynamicSmemBytes = PL::SMEM;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, DEQ>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM);
+  auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, DEQ, XS>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM_MAX);
   if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k, prm);
   return e;
+}
+
+// Runtime part of the shared-memory plan: stage x' in shared memory when it fits beside at least
+// one ring stage per warp (opt-in: QP_XS=1), then as many ring stages (<= 4) as fit.
+int env_no_xs();
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ>
+cudaError_t launch_plan(const GemvParams& prm0, int grid, bool pdl, cudaStream_t s) {
+  using PL = Plan<MODE, CLO, CHI, TB, REPS, false>;
+  using PX = Plan<MODE, CLO, CHI, TB, REPS, true>;
+  GemvParams prm = prm0;
+  const int rs = xs_row_stride(prm.d_in);
+  const int xs_bytes = ((prm.batch * rs + 127) / 128) * 128;
+  if (!DEQ && !env_no_xs() && xs_bytes + PX::NWARP * PX::STAGE <= PX::AVAIL) {
+    prm.xs_bytes = xs_bytes;
+    prm.xs_rs = rs;
+    prm.ns = (std::min)(4, (PX::AVAIL - xs_bytes) / (PX::NWARP * PX::STAGE));
+    return launch_one<MODE, CLO, CHI, L, TB, REPS, false, true>(prm, grid, pdl, s);
+  }
+  prm.xs_bytes = 0;
+  prm.xs_rs = 0;
+  prm.ns = (std::min)(4, PL::AVAIL / (PL::NWARP * PL::STAGE));
+  return launch_one<MODE, CLO, CHI, L, TB, REPS, DEQ, false>(prm, grid, pdl, s);
 }
 
 template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool UNUSED = false>

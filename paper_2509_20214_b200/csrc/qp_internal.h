@@ -55,6 +55,10 @@ struct GemvParams {
   int y_f32;                   // 1: fp32 output, 0: fp16 output
   int y_atomic;                // 1: y was zeroed; CTAs sharing a row tile red.add their scaled partials
   uint32_t zero;               // always 0 (an operand the compiler cannot constant-fold)
+  // shared-memory plan chosen at launch (qp_gemv.cuh launch_plan)
+  int ns;                      // code-ring stages per warp (1..4)
+  int xs_rs;                   // x' staged in shared memory: row stride in bytes (0 = registers)
+  int xs_bytes;                // bytes of the staged x' region (batch rows)
   // cross-CTA fixup workspace
   float* ws;                   // [grid][256] cross-CTA partials (slot = contributing CTA)
   int* counters;               // [RT], zero between launches (self-resetting)

@@ -192,11 +192,13 @@ cudaError_t launch_gather_permute(const void* src, void* dst, int world, int bat
   return cudaGetLastError();
 }
 
-int tune_nwarp() {
+int env_no_xs() {
+  // x' staged in shared memory is opt-in (QP_XS=1): measured slower than the register path on
+  // the C2 shapes (profiles/r1/ab_xs_r1.md)
   static int n = -1;
   if (n < 0) {
-    const char* e = getenv("QP_NWARP");
-    n = e ? atoi(e) : 0;
+    const char* e = getenv("QP_XS");
+    n = (e && atoi(e) != 0) ? 0 : 1;
   }
   return n;
 }

@@ -1,0 +1,17 @@
+# robust A/B over variants "name:lib.so:ENV=val ...": bash scripts/ab4.sh <out> "A:libqpalette.so:QP_NO_XS=1" ...
+out=$1; shift
+mkdir -p gpurun_out
+: > gpurun_out/${out}.txt
+for round in 1 2 3; do
+ for cfg in 4096x4096:tcq:10 4096x4096:half_tcq:13 4096x4096:tcq:16 14336x4096:tcq:10 14336x4096:half_tcq:13 14336x4096:tcq:16 \
+            4096x14336:tcq:10 4096x14336:half_tcq:13 4096x14336:tcq:16 14336x4096:vq:8 14336x4096:nuq:16 14336x4096:vq:12; do
+  IFS=: read sh sc x4 <<< "$cfg"
+  for v in "$@"; do
+   IFS=: read name lib envs <<< "$v"
+   r=$(env QP_LIB_PATH=$PWD/paper_2509_20214_b200/$lib $envs python tools/prof_gemv.py --shape $sh --scheme $sc --bits-x4 $x4 --time --pdl ${QP_AB_ARGS:-} 2>&1 | tail -1)
+   echo "$name | $r" >> gpurun_out/${out}.txt
+  done
+ done
+done
+python tools/ab_summary.py gpurun_out/${out}.txt > gpurun_out/${out}_summary.txt 2>&1
+exit 0
