@@ -421,11 +421,15 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f16", "data": "synthetic",
             "config": {"workload": "C2: Llama-3.1-8B (4096x4096, 14336x4096, 4096x14336) x TCQ-2.5 / half-TCQ-3.25 / "
-                                   "TCQ-4.0 (L=16), RHT + fused dequant-GEMV per layer",
+                                   "TCQ-4.0 (L=16), rotation + fused dequant-GEMV per layer (qp_linear_fwd on raw x)",
                        "batch": batch, "layers_per_step": n_layers, "us_per_layer": round(ms * 1e3 / n_layers, 3),
                        "parallelism": f"row-shard x{world} + NCCL all-gather" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (2 replicas, 326 MB per 2 steps, L2 126 MB)",
-                       "graph": "CUDA graph per step, PDL between the rotation and GEMV kernels",
+                       "graph": "CUDA graph per step, PDL between consecutive kernels",
+                       "kernels_per_layer": round(launches_per_step / n_layers, 3),
+                       "rotation": ("fused into the GEMV kernel (every CTA computes R x in shared memory)"
+                                    if launches_per_step == n_layers else
+                                    "separate rotation kernel before the GEMV kernel"),
                        "gemv_us_per_layer": per_layer_us},
             "roofline": {"bound": "hbm", "achieved": round(gemv_achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(gemv_achieved / peak, 4),

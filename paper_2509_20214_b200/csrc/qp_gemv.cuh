@@ -23,6 +23,7 @@
 //  * Programmatic dependent launch: table build and the first code loads happen before
 //    griddepcontrol.wait (they read only immutable layer data).
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <algorithm>
 #include <utility>
@@ -186,7 +187,8 @@ __device__ __forceinline__ void load_x8(uint32_t* dst, const __half* src) {   //
 // x' B fragments: xb[0..15] (kappa 0..7) and xb[16..31] (kappa 8..15). The second half of this
 // tile's activations (x_hi) is loaded when the tile starts and the first half of the next tile's
 // (x_next) once kappa 0..7 are done, so activation loads never sit on the critical path and
-// need no extra registers. Lanes with no batch row (x_hi == nullptr) keep zeros.
+// need no extra registers. Lanes with no batch row (x_hi == nullptr) keep zeros (loading a valid
+// row for them instead measured 10-25% slower: profiles/r1/ab_xs_r1.md section 4).
 #ifdef QP_ACC4
 constexpr int kAccSets = 2;   // independent accumulator chains per row block (k-step parity)
 #else
@@ -300,7 +302,10 @@ struct Plan {
   static constexpr int STAGE = 512 * CMAX;
   // register budget (128 regs x 512 threads, no spills); x' in shared memory frees the 32
   // B-fragment registers (QP_XS_WARPS experiments with more warps)
-  static constexpr int NWARP = CMAX <= 6 ? (XS ? QP_XS_WARPS : 16) : 12;
+#ifndef QP_WIDE_CMAX
+#define QP_WIDE_CMAX 6
+#endif
+  static constexpr int NWARP = CMAX <= QP_WIDE_CMAX ? (XS ? QP_XS_WARPS : 16) : 12;
   static constexpr int BAR_OFF = TAB;
   static constexpr int XS_OFF = TAB + 1024;
   static constexpr int PART = NWARP * 2 * 256 * 4;  // epilogue warp partials
@@ -334,9 +339,112 @@ __device__ __forceinline__ void store_out(const GemvParams& p, int rt, int row, 
 }
 
 
-template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, bool XS>
-__global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32, 1)
+
+// ---- fused activation rotation (XM == 2) --------------------------------------------------
+// x' = (1/sqrt(b)) blockdiag(H_b) D x computed by every CTA into its staged x'.
+// The arithmetic is that of qp_rht_kernel<8> step for step (3 butterfly stages in registers,
+// 5 across lanes, the rest through shared memory, fp32, one RNE rounding), so the result is
+// bitwise the one the separate rotation kernel writes. A warp owns a 256-element segment; a round
+// transforms NWARP / (b/256) blocks; the scratch holds one fp32 block per concurrently processed
+// block (NWARP * 256 floats).
+__host__ __device__ constexpr int rot_scratch_offset(int batch, int rs) { return ((batch * rs + 127) / 128) * 128; }
+
+template <int NWARP>
+__device__ __forceinline__ void rotate_x(const GemvParams& p, uint8_t* xs, float* scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bsz = p.rht_block, spb = bsz >> 8;          // 256-element segments per block
+  const int bpr = NWARP / spb;                          // blocks per round
+  const int nblk = p.d_in / bsz, total = p.batch * nblk;
+  const int slot = warp / spb, seg = warp - slot * spb;
+  const int e0 = seg * 256 + lane * 8;                  // first element of this lane in its block
+  for (int r0 = 0; r0 < total; r0 += bpr) {
+    const int gb = r0 + slot;
+    const bool act = slot < bpr && gb < total;
+    const int beta = act ? gb / nblk : 0, blk = act ? gb - beta * nblk : 0;
+    float v[8];
+    if (act) {
+      const size_t base = (size_t)beta * p.d_in + (size_t)blk * bsz + e0;
+      if (p.x_dtype == 0) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.x_raw) + base));
+        const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __half22float2(h[k]);
+          v[2 * k] = f.x;
+          v[2 * k + 1] = f.y;
+        }
+      } else if (p.x_dtype == 1) {
+        const __nv_bfloat16* xb16 = reinterpret_cast<const __nv_bfloat16*>(p.x_raw) + base;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(xb16[i]);
+      } else {
+        const float4 f0 = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.x_raw) + base));
+        const float4 f1 = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.x_raw) + base) + 1);
+        v[0] = f0.x; v[1] = f0.y; v[2] = f0.z; v[3] = f0.w; v[4] = f1.x; v[5] = f1.y; v[6] = f1.z; v[7] = f1.w;
+      }
+      const int gi = blk * bsz + e0;                    // index within the row (8 | gi: one sign word)
+      const uint32_t sw = __ldg(p.rht_signs + (gi >> 5)) >> (gi & 31);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if ((sw >> i) & 1u) v[i] = -v[i];
+#pragma unroll
+      for (int h = 1; h < 8; h <<= 1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if ((i & h) == 0) {
+            const float a0 = v[i], a1 = v[i + h];
+            v[i] = a0 + a1;
+            v[i + h] = a0 - a1;
+          }
+    }
+    // lane stages (all lanes of an active warp are active)
+    if (slot < bpr && r0 + slot < total) {
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const bool upper = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float o = __shfl_xor_sync(0xffffffffu, v[i], m);
+          v[i] = upper ? (o - v[i]) : (v[i] + o);
+        }
+      }
+    }
+    float* sb = scratch + slot * bsz;
+    for (int h = 256; h < bsz; h <<= 1) {
+      __syncthreads();
+      if (act)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sb[e0 + i] = v[i];
+      __syncthreads();
+      if (act)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int k = e0 + i;
+          const float o = sb[k ^ h];
+          v[i] = (k & h) ? (o - v[i]) : (v[i] + o);
+        }
+    }
+    if (act) {
+      uint32_t hw[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const __half2 h2 = __floats2half2_rn(v[2 * k] * p.rht_scale, v[2 * k + 1] * p.rht_scale);
+        hw[k] = *reinterpret_cast<const uint32_t*>(&h2);
+      }
+      const int k = blk * bsz + e0;
+      uint8_t* dst = xs + beta * p.xs_rs + (k >> 6) * 136 + (k & 63) * 2;
+      *reinterpret_cast<uint2*>(dst) = make_uint2(hw[0], hw[1]);
+      *reinterpret_cast<uint2*>(dst + 8) = make_uint2(hw[2], hw[3]);
+    }
+  }
+}
+
+// XM: 0 = x' B fragments from global into registers, 1 = x' staged in shared memory,
+//     2 = x' computed in shared memory by every CTA from raw x (fused rotation) + in-kernel zeroing
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, int XM>
+__global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWARP * 32, 1)
     qp_gemv_kernel(const __grid_constant__ GemvParams p) {
+  constexpr bool XS = XM != 0;
   using PL = Plan<MODE, CLO, CHI, TB, REPS, XS>;
   constexpr int CMAX = PL::CMAX, NWARP = PL::NWARP;
   const int NS = p.ns;
@@ -360,6 +468,9 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32
   auto flush_stamps = [](int) {};
 #endif
   stamp(0);
+  // the compact table words first: their L2 latency then overlaps the rest of the prologue
+  TableBuild<REPS, NWARP * 32, PL::ENTRIES> tb;
+  tb.load(p.table);
   const int g = lane >> 2, q = lane & 3;
   // tile indices are 32-bit: the host guarantees RT*KT*gridDim < 2^32
   const uint32_t N = (uint32_t)p.RT * (uint32_t)p.KT;
@@ -377,17 +488,25 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32
   const uint32_t ring = smem_u32(smem + PL::XS_OFF + p.xs_bytes) + (uint32_t)(warp * NS * PL::STAGE);
   const uint32_t bars = smem_u32(smem + PL::BAR_OFF) + (uint32_t)(warp * NS * 8);
   uint64_t pol = 0;
-  // issue the copy of tile t (row tile rt_, k tile kt_) into stage st (lane 0 only)
-  auto fetch = [&](uint32_t rt_, int kt_, int st, uint32_t dep = 0u) {
-    const int c = (CLO == CHI || kt_ < KH) ? CLO : CHI;
-    const long long off = (long long)rt_ * rowtile_bytes +
-                          (kt_ < KH ? (long long)kt_ * 512 * CLO : (long long)KH * 512 * CLO + (long long)(kt_ - KH) * 512 * CHI);
+  // bytes of k tile kt_ (half-TCQ: c_lo on the first KT/2 k tiles, c_hi on the rest)
+  auto tile_bytes = [&](int kt_) -> uint32_t { return 512u * ((CLO == CHI || kt_ < KH) ? CLO : CHI); };
+  // issue the copy of the tile at `src` into stage st (lane 0 only)
+  auto fetch = [&](const uint8_t* src, uint32_t nbytes, int st, uint32_t dep = 0u) {
     const uint32_t bar = bars + 8u * st;
-    mbar_expect_tx(bar, 512u * c);
-    bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, p.codes + off, 512u * c, bar, pol);
+    mbar_expect_tx(bar, nbytes);
+    bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, src, nbytes, bar, pol);
   };
   uint32_t rt = div_kt(a);
   int kt = (int)(a - rt * KT);
+  // the refill cursor: the next tile to be fetched (its address advances by whole tiles: the
+  // LAYOUT.md stream is row-tile-major, tiles of a row tile in k order, all contiguous)
+  const uint8_t* f_ptr = p.codes + (long long)rt * rowtile_bytes +
+                         (kt < KH ? (long long)kt * 512 * CLO : (long long)KH * 512 * CLO + (long long)(kt - KH) * 512 * CHI);
+  int kt_f = kt;
+  auto advance_f = [&]() {
+    f_ptr += tile_bytes(kt_f);
+    if (++kt_f == (int)KT) kt_f = 0;
+  };
   if (lane == 0) {
 #pragma unroll
     for (int st = 0; st < NS; ++st) mbar_init(bars + 8u * st, 1);
@@ -395,11 +514,9 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32
     pol = l2_evict_first_policy();
     // only the first tile now: the whole grid's first-wave requests then complete before the
     // second wave (issued after the table build) competes with them for HBM
-    if (a < b) fetch(rt, kt, 0);
+    if (a < b) fetch(f_ptr, tile_bytes(kt_f), 0);
   }
-  // the tile NS ahead of the current one (refill target)
-  uint32_t rt_f = rt + div_kt((uint32_t)(kt + NS));
-  int kt_f = (int)((uint32_t)(kt + NS) - div_kt((uint32_t)(kt + NS)) * KT);
+  advance_f();
 
   // per-row scales of the current row tile, rows g, g+8, g+16, g+24 (prefetched into registers
   // when a row tile starts; consumed when its partial is flushed)
@@ -420,28 +537,19 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32
   // Everything up to griddepcontrol.wait reads only immutable layer data, so under programmatic
   // dependent launch it overlaps the previous kernel: the code copies are in flight (issued
   // above) while the table words arrive from L2 and are expanded into the replicated image.
-  {
-    TableBuild<REPS, NWARP * 32, PL::ENTRIES> tb;
-    tb.load(p.table);
-    stamp(7);
-    tb.store(tab);
-  }
+  stamp(7);
+  tb.store(tab);
   stamp(6);
-  if (lane == 0) {                                 // the rest of the ring's first fill
-    uint32_t r_ = rt;
-    int k_ = kt;
-#pragma unroll
-    for (int st = 1; st < NS; ++st) {
-      if (++k_ == (int)KT) { k_ = 0; ++r_; }
-      if (a + st < b) fetch(r_, k_, st);
-    }
+  for (int st = 1; st < NS; ++st) {                // the rest of the ring's first fill
+    if (lane == 0 && a + st < b) fetch(f_ptr, tile_bytes(kt_f), st);
+    advance_f();
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   stamp(5);
   // this lane's x' row in the staged copy (lanes without a batch row read row batch-1: their
   // products land in y columns that are never stored)
   const uint32_t xs_lane = smem_u32(smem + PL::XS_OFF) + (uint32_t)(min(g, p.batch - 1) * p.xs_rs + q * 136);
-  if constexpr (XS) {
+  if constexpr (XM == 1) {
     // x' (the previous kernel's output) -> padded shared layout, 8 bytes per thread-step
     const int units = p.d_in / 4;                  // 8-byte units per row
     for (int i = tid; i < p.batch * units; i += NWARP * 32) {
@@ -449,6 +557,34 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32
       const uint2 v = __ldg(reinterpret_cast<const uint2*>(p.x + (size_t)row * p.d_in + k));
       *reinterpret_cast<uint2*>(smem + PL::XS_OFF + row * p.xs_rs + (k >> 6) * 136 + (k & 63) * 2) = v;
     }
+  } else if constexpr (XM == 2) {
+    if (p.zero_y) {
+      // this CTA's share of the fp32 outputs, then arrive on the grid counter; every CTA waits for
+      // all arrivals before its first write to y (first_write below)
+      const long long gstride = (long long)gridDim.x * NWARP * 32, gme = (long long)blockIdx.x * NWARP * 32 + tid;
+      for (int i = 0; i < p.n_out; ++i) {
+        const int rows = (p.rt_begin[i + 1] - p.rt_begin[i]) * kTileRows;
+        const long long n = (long long)p.batch * rows;
+        float* y = reinterpret_cast<float*>(p.y[i]);
+        for (long long e = gme; e < n; e += gstride) {
+          const int bb = (int)(e / rows);
+          y[(size_t)bb * p.ldy[i] + (e - (long long)bb * rows)] = 0.f;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int gen0;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(gen0) : "l"(p.bar_count + 1) : "memory");
+        *reinterpret_cast<int*>(smem + PL::BAR_OFF + 1020) = gen0;   // last word of the mbarrier area
+        __threadfence();
+        if (atomicAdd(p.bar_count, 1) == (int)gridDim.x - 1) {
+          p.bar_count[0] = 0;                      // every CTA has arrived: reset, open the barrier
+          __threadfence();
+          atomicAdd(p.bar_count + 1, 1);
+        }
+      }
+    }
+    rotate_x<NWARP>(p, smem + PL::XS_OFF, reinterpret_cast<float*>(smem + PL::XS_OFF + rot_scratch_offset(p.batch, p.xs_rs)));
   } else if (xrow && a < b) {                      // first tile, kappa 0..7
     load_x8(xb, xlane + kt * kTileCols);
     load_x8(xb + 8, xlane + kt * kTileCols + 16);
@@ -467,6 +603,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32
 
   float hp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};   // head row-tile partial
   uint32_t cur[4 * CMAX];
+  bool y_open = false;                             // XM == 2: the in-kernel zeroing of y is done
   int st = 0;
   uint32_t par = 0;
   for (uint32_t t = a; t < b; ++t) {
@@ -487,8 +624,8 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32
       // makes lane 0's refill depend on all of them (p.zero == 0 keeps the value unchanged).
       const uint32_t last = (CLO == CHI || c == CMAX) ? cur[4 * CMAX - 1] : cur[4 * CLO - 1];
       const uint32_t dep = __reduce_or_sync(0xffffffffu, last & p.zero);
-      if (lane == 0 && t + NS < b) fetch(rt_f, kt_f, st, dep);
-      if (++kt_f == (int)KT) { kt_f = 0; ++rt_f; }
+      if (lane == 0 && t + NS < b) fetch(f_ptr, tile_bytes(kt_f), st, dep);
+      advance_f();
     }
     int kt_n = kt + 1;
     uint32_t rt_n = rt;
@@ -510,6 +647,22 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32
 
     if constexpr (!DEQ) {
       if (kt == (int)KT - 1 || t == b - 1) {
+        if constexpr (XM == 2) {
+          // the grid's in-kernel zeroing of y must be complete before this warp's first write
+          if (p.zero_y && !y_open) {
+            if (lane == 0) {
+              const int gen0 = *reinterpret_cast<const int*>(smem + PL::BAR_OFF + 1020);
+              int gen;
+              for (;;) {
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(gen) : "l"(p.bar_count + 1) : "memory");
+                if (gen != gen0) break;
+                __nanosleep(32);
+              }
+            }
+            __syncwarp();
+            y_open = true;
+          }
+        }
         if constexpr (kAccSets == 2) {
 #pragma unroll
           for (int m = 0; m < 2; ++m)
@@ -681,9 +834,9 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, XS>::NWARP * 32
   flush_stamps(8);
 }
 
-template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, bool XS>
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, int XM>
 cudaError_t launch_one(const GemvParams& prm, int grid, bool pdl, cudaStream_t s) {
-  using PL = Plan<MODE, CLO, CHI, TB, REPS, XS>;
+  using PL = Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>;
   const int smem = PL::XS_OFF + (std::max)(prm.xs_bytes + PL::NWARP * prm.ns * PL::STAGE, PL::PART);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -695,7 +848,7 @@ cudaError_t launch_one(const GemvParams& prm, int grid, bool pdl, cudaStream_t s
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, DEQ, XS>;
+  auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, DEQ, XM>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM_MAX);
   if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k, prm);
   return e;
@@ -704,23 +857,37 @@ cudaError_t launch_one(const GemvParams& prm, int grid, bool pdl, cudaStream_t s
 // Runtime part of the shared-memory plan: stage x' in shared memory when it fits beside at least
 // one ring stage per warp (opt-in: QP_XS=1), then as many ring stages (<= 4) as fit.
 int env_no_xs();
+constexpr int kMaxRotRounds = 4;   // fused rotation: most rounds of in-CTA transforms worth doing
 template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ>
 cudaError_t launch_plan(const GemvParams& prm0, int grid, bool pdl, cudaStream_t s) {
   using PL = Plan<MODE, CLO, CHI, TB, REPS, false>;
   using PX = Plan<MODE, CLO, CHI, TB, REPS, true>;
   GemvParams prm = prm0;
   const int rs = xs_row_stride(prm.d_in);
-  const int xs_bytes = ((prm.batch * rs + 127) / 128) * 128;
+  const int xs_bytes = rot_scratch_offset(prm.batch, rs);
+  if (!DEQ && prm.x_raw) {
+    // fused rotation: x' and the rotation scratch beside >= 1 ring stage per warp, and at most
+    // kMaxRotRounds rounds of NWARP / (b/256) blocks (else the caller launches the rotation kernel)
+    const int spb = prm.rht_block / 256;
+    const int scratch = prm.rht_block > 256 ? PX::NWARP * 256 * 4 : 0;
+    const int rounds = spb >= 1 && spb <= PX::NWARP ? (prm.batch * (prm.d_in / prm.rht_block) + PX::NWARP / spb - 1) /
+                                                          (PX::NWARP / spb) : 1 << 20;
+    if (rounds > kMaxRotRounds || xs_bytes + scratch + PX::NWARP * PX::STAGE > PX::AVAIL) return cudaErrorNotSupported;
+    prm.xs_bytes = xs_bytes + scratch;
+    prm.xs_rs = rs;
+    prm.ns = (std::min)(4, (PX::AVAIL - prm.xs_bytes) / (PX::NWARP * PX::STAGE));
+    return launch_one<MODE, CLO, CHI, L, TB, REPS, false, 2>(prm, grid, pdl, s);
+  }
   if (!DEQ && !env_no_xs() && xs_bytes + PX::NWARP * PX::STAGE <= PX::AVAIL) {
     prm.xs_bytes = xs_bytes;
     prm.xs_rs = rs;
     prm.ns = (std::min)(4, (PX::AVAIL - xs_bytes) / (PX::NWARP * PX::STAGE));
-    return launch_one<MODE, CLO, CHI, L, TB, REPS, false, true>(prm, grid, pdl, s);
+    return launch_one<MODE, CLO, CHI, L, TB, REPS, false, 1>(prm, grid, pdl, s);
   }
   prm.xs_bytes = 0;
   prm.xs_rs = 0;
   prm.ns = (std::min)(4, PL::AVAIL / (PL::NWARP * PL::STAGE));
-  return launch_one<MODE, CLO, CHI, L, TB, REPS, DEQ, false>(prm, grid, pdl, s);
+  return launch_one<MODE, CLO, CHI, L, TB, REPS, DEQ, 0>(prm, grid, pdl, s);
 }
 
 template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool UNUSED = false>

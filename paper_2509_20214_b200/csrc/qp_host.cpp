@@ -78,6 +78,15 @@ bool pdl_disabled_by_env() {
   return off;
 }
 
+bool fused_rht_disabled_by_env() {   // QP_FUSED_RHT=0: always launch the separate rotation kernel
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QP_FUSED_RHT");
+    v = (e && atoi(e) == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -271,11 +280,11 @@ qp_status layer_init(qp_layer* l, int d_out, int d_in, qp_scheme scheme, int bit
   l->d_codes = static_cast<uint8_t*>(dev_alloc(l->code_bytes));
   l->d_scales = static_cast<float*>(dev_alloc((size_t)d_out * 4));
   l->d_ws = static_cast<float*>(dev_alloc((size_t)l->grid * 256 * 4));
-  l->d_counters = static_cast<int*>(dev_alloc((size_t)(d_out / kTileRows) * 4));
+  l->d_counters = static_cast<int*>(dev_alloc((size_t)(d_out / kTileRows + 2) * 4));   // + grid barrier [2]
   l->d_xrot = static_cast<__half*>(dev_alloc((size_t)8 * d_in * 2));
   if (!l->d_codes || !l->d_scales || !l->d_ws || !l->d_counters || !l->d_xrot)
     return fail(QP_ERR_ALLOC, "device allocation of %zu code bytes failed", l->code_bytes);
-  CUDA_TRY(cudaMemset(l->d_counters, 0, (size_t)(d_out / kTileRows) * 4), "cudaMemset(counters)");
+  CUDA_TRY(cudaMemset(l->d_counters, 0, (size_t)(d_out / kTileRows + 2) * 4), "cudaMemset(counters)");
   return QP_OK;
 }
 
@@ -333,9 +342,29 @@ int zero_ctas(const long long* zn, int n) {
 // side_ctas: CTAs of the preceding rotation / zeroing kernel. Under PDL the GEMV (one CTA per SM,
 // the whole register file) cannot share an SM with them, so a GEMV CTA placed there would start
 // its prologue only after they exit and finish last; the GEMV leaves those SMs to them instead.
+// Fused rotation request for run_gemv: x' = R x computed inside the GEMV kernel (and, for the
+// fp32 atomic path, y zeroed there too); run_gemv reports `unsupported` (nothing launched) when
+// the layer / batch does not fit the fused plan, and the caller launches the rotation kernel.
+struct FusedRot {
+  const qp_rht* r;
+  const void* x;
+  qp_dtype xt;
+  bool zero_y;
+};
+
 qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, const int* rt_begin, void* const* ys,
-                   const int* ldy, qp_dtype yt, bool pdl, cudaStream_t s, bool y_atomic, int side_ctas = 0) {
+                   const int* ldy, qp_dtype yt, bool pdl, cudaStream_t s, bool y_atomic, int side_ctas = 0,
+                   const FusedRot* fr = nullptr, bool* unsupported = nullptr) {
   GemvParams p{};
+  if (fr) {
+    p.x_raw = fr->x;
+    p.x_dtype = (int)fr->xt;
+    p.rht_block = fr->r->block;
+    p.rht_signs = fr->r->d_signs;
+    p.rht_scale = (float)(1.0 / std::sqrt((double)fr->r->block));
+    p.zero_y = fr->zero_y ? 1 : 0;
+    p.bar_count = l->d_counters + l->d_out / kTileRows;
+  }
   p.y_atomic = y_atomic ? 1 : 0;
   p.codes = l->d_codes;
   p.scales = l->d_scales;
@@ -363,6 +392,10 @@ qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, co
   if (pdl && side_ctas > 0 && side_ctas <= kMaxSideCtas) grid = std::max(1, std::min(grid, num_sms() - side_ctas));
   set_magics(p, grid);
   cudaError_t e = l->launcher(p, grid, 0, false, pdl, s);
+  if (e == cudaErrorNotSupported && fr && unsupported) {
+    *unsupported = true;
+    return QP_OK;
+  }
   if (e != cudaSuccess) return cuda_fail(e, "fused dequant-GEMV launch");
   count_launch();
   if (tl) {
@@ -641,6 +674,15 @@ qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch
   // a row tile add into it; QP_DETERMINISTIC or fp16 output: in-order cross-CTA reduction instead
   const bool atomic = yt == QP_F32 && !(flags & QP_DETERMINISTIC);
   const long long zn[1] = {(long long)batch * l->d_out};
+  const int rtb[2] = {0, l->d_out / kTileRows};
+  const int ldy[1] = {l->d_out};
+  if (!(flags & QP_X_PREROTATED) && !(flags & QP_SEPARATE_RHT) && !fused_rht_disabled_by_env()) {
+    // one kernel: every CTA rotates x itself (and zeroes y) -- no rotation kernel on the path
+    const FusedRot fr{l->rht, x, xt, atomic && !(flags & QP_Y_ACCUMULATE)};
+    bool unsup = false;
+    st = run_gemv(l, nullptr, batch, 1, rtb, ys, ldy, yt, pdl, s, atomic, 0, &fr, &unsup);
+    if (st != QP_OK || !unsup) return st;
+  }
   int side = 0;
   if (!(flags & QP_X_PREROTATED)) {
     const int nz = atomic && !(flags & QP_Y_ACCUMULATE) ? 1 : 0;
@@ -656,8 +698,6 @@ qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch
     cudaError_t e = launch_zero(zp, side, pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "zero kernel launch");
   }
-  const int rtb[2] = {0, l->d_out / kTileRows};
-  const int ldy[1] = {l->d_out};
   return run_gemv(l, xr, batch, 1, rtb, ys, ldy, yt, pdl, s, atomic, side);
 }
 
@@ -743,6 +783,19 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
   const bool atomic = yt == QP_F32 && !(flags & QP_DETERMINISTIC);
   long long zn[kMaxGroup];
   for (int i = 0; i < n; ++i) zn[i] = (long long)batch * g->d_outs[i];
+  int rtb[kMaxGroup + 1];
+  int ldy[kMaxGroup];
+  rtb[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    rtb[i + 1] = rtb[i] + g->d_outs[i] / kTileRows;
+    ldy[i] = g->d_outs[i];
+  }
+  if (!(flags & QP_X_PREROTATED) && !(flags & QP_SEPARATE_RHT) && !fused_rht_disabled_by_env()) {
+    const FusedRot fr{l->rht, x, xt, atomic && !(flags & QP_Y_ACCUMULATE)};
+    bool unsup = false;
+    st = run_gemv(l, nullptr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic, 0, &fr, &unsup);
+    if (st != QP_OK || !unsup) return st;
+  }
   int side = 0;
   if (!(flags & QP_X_PREROTATED)) {
     const int nz = atomic && !(flags & QP_Y_ACCUMULATE) ? n : 0;
@@ -759,13 +812,6 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
     side = zero_ctas(zn, n);
     cudaError_t e = launch_zero(zp, side, !(flags & QP_NO_PDL), s);
     if (e != cudaSuccess) return cuda_fail(e, "zero kernel launch");
-  }
-  int rtb[kMaxGroup + 1];
-  int ldy[kMaxGroup];
-  rtb[0] = 0;
-  for (int i = 0; i < n; ++i) {
-    rtb[i + 1] = rtb[i] + g->d_outs[i] / kTileRows;
-    ldy[i] = g->d_outs[i];
   }
   return run_gemv(l, xr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic, side);
 }

@@ -58,7 +58,16 @@ struct GemvParams {
   // shared-memory plan chosen at launch (qp_gemv.cuh launch_plan)
   int ns;                      // code-ring stages per warp (1..4)
   int xs_rs;                   // x' staged in shared memory: row stride in bytes (0 = registers)
-  int xs_bytes;                // bytes of the staged x' region (batch rows)
+  int xs_bytes;                // bytes of the staged x' region (+ the fused rotation's scratch)
+  // fused activation rotation (x' = (1/sqrt(b)) blockdiag(H_b) D x computed by every CTA into its
+  // staged x') and in-kernel zeroing of y, replacing the separate rotation kernel
+  const void* x_raw;           // raw x [batch][d_in] (nullptr: x above is already x')
+  int x_dtype;                 // 0 f16, 1 bf16, 2 f32
+  int rht_block;               // b (power of two dividing d_in)
+  const uint32_t* rht_signs;   // d_in bits, 1 = negative
+  float rht_scale;             // 1/sqrt(b)
+  int zero_y;                  // 1: zero the fp32 outputs in-kernel before accumulating into them
+  int* bar_count;              // [2] grid arrival counter + generation (self-resetting)
   // cross-CTA fixup workspace
   float* ws;                   // [grid][256] cross-CTA partials (slot = contributing CTA)
   int* counters;               // [RT], zero between launches (self-resetting)

@@ -327,3 +327,74 @@ def test_y_accumulate_flag():
         lay.forward(xg, 3, torch.empty(3, 1024, dtype=torch.float16, device="cuda"), flags=Lb.QP_Y_ACCUMULATE)
     with pytest.raises(Lb.QPError):
         lay.forward(xg, 3, torch.empty(3, 1024, device="cuda"), flags=Lb.QP_Y_ACCUMULATE | Lb.QP_DETERMINISTIC)
+
+
+@pytest.mark.parametrize("d_out,d_in,scheme,bits_x4,batch", [
+    (256, 4096, "tcq", 10, 1), (256, 4096, "tcq", 10, 2), (320, 14336, "half_tcq", 13, 1),
+    (96, 1536, "vq", 8, 3), (64, 256, "tcq", 16, 8), (128, 28672, "nuq", 16, 1), (96, 2048, "tcq", 16, 4),
+])
+@pytest.mark.parametrize("x_dtype", [torch.float16, torch.bfloat16, torch.float32])
+def test_fused_rotation_path(d_out, d_in, scheme, bits_x4, batch, x_dtype):
+    """Default qp_linear_fwd fuses the rotation into the GEMV kernel when x' fits its plan (one
+    launch; y zeroed in-kernel); QP_SEPARATE_RHT forces rotation kernel + GEMV. Both meet the
+    oracle bar and agree with each other (x' is bitwise the same; only the atomic summation order
+    of split row tiles differs)."""
+    Lb = _need_gpu()
+    lay, codes, s, ocb = _layer(scheme, bits_x4, d_out, d_in, layer_id=21)
+    x = activations_fp16(batch, d_in)
+    xin = x.astype(np.float64)
+    if x_dtype != torch.float16:    # the oracle sees the same (rounded) input values
+        xin = torch.from_numpy(x).to(x_dtype).float().numpy().astype(np.float64)
+    y_ref = linear.linear_from_codes(codes, d_out, d_in, scheme, bits_x4, ocb, s, xin, SEED)
+    n0 = Lb.launch_count()
+    y_f = _fwd(lay, x, batch, x_dtype=x_dtype)
+    n_fused = Lb.launch_count() - n0
+    n0 = Lb.launch_count()
+    y_s = _fwd(lay, x, batch, x_dtype=x_dtype, flags=Lb.QP_SEPARATE_RHT)
+    n_sep = Lb.launch_count() - n0
+    assert n_sep == 2 and n_fused in (1, 2)
+    for y in (y_f, y_s):
+        assert np.max(linear.normwise_error(y, y_ref)) <= TOL
+    assert np.max(np.abs(y_f - y_s)) <= 1e-5 * np.max(np.abs(y_s))
+    # fp16 output (in-order reduction, no zeroing) and y accumulate through the fused path
+    y16 = _fwd(lay, x, batch, y_dtype=torch.float16, x_dtype=x_dtype)
+    assert np.max(linear.normwise_error(y16, y_ref)) <= TOL
+    xt = torch.from_numpy(x).to("cuda", x_dtype)
+    y = torch.full((batch, d_out), 0.25, device="cuda")
+    lay.forward(xt, batch, y, flags=Lb.QP_Y_ACCUMULATE)
+    lay.forward(xt, batch, y, flags=Lb.QP_Y_ACCUMULATE)
+    torch.cuda.synchronize()
+    assert np.max(linear.normwise_error(y.cpu().numpy() - 0.25, 2 * y_ref)) <= TOL
+
+
+def test_fused_rotation_is_single_kernel_at_batch1():
+    """The C2 shapes at batch 1 take the one-kernel path (the bench's step)."""
+    Lb = _need_gpu()
+    for d_out, d_in in ((4096, 4096), (1024, 14336)):
+        lay, _, _, _ = _layer("tcq", 10, d_out, d_in, layer_id=22)
+        x = activations_fp16(1, d_in)
+        n0 = Lb.launch_count()
+        _fwd(lay, x, 1)
+        assert Lb.launch_count() - n0 == 1
+
+
+def test_fused_rotation_repeated_launches_in_graph():
+    """The in-kernel zeroing barrier is self-resetting: many back-to-back launches (captured in
+    a CUDA graph, as the bench runs them) keep producing the same y."""
+    Lb = _need_gpu()
+    lay, codes, s, ocb = _layer("tcq", 10, 2048, 4096, layer_id=23)
+    x = torch.from_numpy(activations_fp16(1, 4096)).cuda()
+    y_ref = linear.linear_from_codes(codes, 2048, 4096, "tcq", 10, ocb, s, x.cpu().numpy().astype(np.float64), SEED)
+    y = torch.empty(1, 2048, device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        lay.forward(x, 1, y, stream=st)
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(16):
+                lay.forward(x, 1, y, stream=st)
+        for _ in range(4):
+            g.replay()
+        st.synchronize()
+    assert np.max(linear.normwise_error(y.cpu().numpy(), y_ref)) <= TOL

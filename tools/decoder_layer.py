@@ -78,10 +78,7 @@ def main():
                                                 cbs[key], rots[d_in]))
             ops.append((members, QL.Group(lays) if len(lays) > 1 else lays[0], lays, d_in))
         reps.append(ops)
-    peak = 6535.1
-    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(pk):
-        peak = float(json.load(open(pk))["hbm_gbs"])
+    peak, _ = P.hbm_peak()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     for batch in [int(b) for b in a.batches.split(",")]:
         xs = {d: torch.from_numpy(activations_fp16(batch, d)).cuda() for d in (H, FF)}

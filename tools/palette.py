@@ -45,3 +45,13 @@ def lut_bytes(scheme: str, bits_x4: int) -> int:
     if scheme == "vq":
         return 4 << (bits_x4 // 2)
     return 2 << (bits_x4 // 4)
+
+
+def hbm_peak() -> tuple[float, str]:
+    """Roofline denominator (GB/s): MEASURED_PEAKS.json's copy bandwidth if the driver wrote it,
+    else the B200_PROFILING.md fallback of 6650 GB/s (same rule as bench.py)."""
+    import json
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        return float(json.load(open(pk))["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"

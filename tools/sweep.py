@@ -80,10 +80,7 @@ def main():
     ap.add_argument("--schemes", default="")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
     a = ap.parse_args()
-    peak = 6535.1
-    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(pk):
-        peak = float(json.load(open(pk))["hbm_gbs"])
+    peak, _ = P.hbm_peak()
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     widths = P.TARGET if a.widths == "target" else P.PALETTE
     if a.schemes:
