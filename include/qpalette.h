@@ -73,9 +73,10 @@ typedef enum { QP_F16 = 0, QP_BF16 = 1, QP_F32 = 2 } qp_dtype;
 #define QP_NO_PDL 2u         /* launch without programmatic dependent launch        */
 #define QP_DETERMINISTIC 4u  /* fp32 y: in-order cross-CTA reduction (bitwise reproducible) instead of
                                 zero-then-atomic-add (fp16 y is always in-order)        */
-#define QP_SEPARATE_RHT 16u /* launch the rotation as its own kernel (qp_rht_apply's) instead of fusing it
-                                into the GEMV kernel; the default fuses it when x' fits the kernel's
-                                shared-memory plan (small batch x d_in), else falls back to this     */
+#define QP_FUSE_RHT 16u    /* compute R x inside the GEMV kernel (every CTA, in shared memory; fp32 y
+                                zeroed in-kernel) instead of launching the rotation kernel, when x'
+                                fits the kernel's plan. Opt-in: on B200 at the C2 shapes the
+                                PDL-overlapped rotation kernel is faster (profiles/r1/ab_xs_r1.md) */
 #define QP_Y_ACCUMULATE 8u  /* fp32 y only: y += diag(s) W_hat R x (y is not zeroed first; e.g. a residual
                                 add). Not with QP_DETERMINISTIC.                                        */
 
@@ -127,9 +128,9 @@ qp_status qp_layer_get_scales(const qp_layer* l, float* scales_host);
 
 /* y[batch][d_out] (device, dtype yt in {F16, F32}) = diag(s) W_hat R x (the fused
  * dequantize-and-multiply). x: device [batch][d_in] of dtype xt, or R x in
- * fp16 with QP_X_PREROTATED. One kernel when x' fits the GEMV's shared-memory plan (every CTA
- * computes R x itself and zeroes fp32 y in-kernel, bitwise the rotation kernel's x'); otherwise,
- * or with QP_SEPARATE_RHT, two kernels: rotation + fused GEMV (PDL-chained). */
+ * fp16 with QP_X_PREROTATED. Two kernels: rotation (+ zeroing of fp32 y) and the fused GEMV,
+ * PDL-chained; with QP_FUSE_RHT one kernel when x' fits its shared-memory plan (every CTA computes
+ * R x itself -- bitwise the rotation kernel's x' -- and zeroes fp32 y in-kernel). */
 qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch, void* y, qp_dtype yt,
                         unsigned flags, void* stream);
 

@@ -26,7 +26,7 @@ QP_X_PREROTATED = 1
 QP_NO_PDL = 2
 QP_DETERMINISTIC = 4
 QP_Y_ACCUMULATE = 8
-QP_SEPARATE_RHT = 16
+QP_FUSE_RHT = 16
 
 # every symbol include/qpalette.h declares (checked by tests/test_abi.py)
 EXPORTS = [

@@ -303,7 +303,7 @@ struct Plan {
   // register budget (128 regs x 512 threads, no spills); x' in shared memory frees the 32
   // B-fragment registers (QP_XS_WARPS experiments with more warps)
 #ifndef QP_WIDE_CMAX
-#define QP_WIDE_CMAX 6
+#define QP_WIDE_CMAX 8   // 16 warps up to c = 8 (4 bits); 12 above (register budget)
 #endif
   static constexpr int NWARP = CMAX <= QP_WIDE_CMAX ? (XS ? QP_XS_WARPS : 16) : 12;
   static constexpr int BAR_OFF = TAB;
@@ -334,7 +334,10 @@ __device__ __forceinline__ void store_out(const GemvParams& p, int rt, int row, 
   while (i + 1 < p.n_out && rt >= p.rt_begin[i + 1]) ++i;
   const int grow = (rt - p.rt_begin[i]) * kTileRows + row;
   v *= scale;
-  if (p.y_f32) reinterpret_cast<float*>(p.y[i])[(size_t)b * p.ldy[i] + grow] = v;
+  if (p.y_f32) {
+    float* dst = reinterpret_cast<float*>(p.y[i]) + (size_t)b * p.ldy[i] + grow;
+    *dst = p.y_accum ? *dst + v : v;        // the owning warp is the only writer of this element
+  }
   else reinterpret_cast<__half*>(p.y[i])[(size_t)b * p.ldy[i] + grow] = __float2half_rn(v);
 }
 
@@ -857,7 +860,7 @@ cudaError_t launch_one(const GemvParams& prm, int grid, bool pdl, cudaStream_t s
 // Runtime part of the shared-memory plan: stage x' in shared memory when it fits beside at least
 // one ring stage per warp (opt-in: QP_XS=1), then as many ring stages (<= 4) as fit.
 int env_no_xs();
-constexpr int kMaxRotRounds = 4;   // fused rotation: most rounds of in-CTA transforms worth doing
+int fused_rht_max_rounds();   // fused rotation: most rounds of in-CTA transforms worth doing
 template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ>
 cudaError_t launch_plan(const GemvParams& prm0, int grid, bool pdl, cudaStream_t s) {
   using PL = Plan<MODE, CLO, CHI, TB, REPS, false>;
@@ -872,7 +875,7 @@ cudaError_t launch_plan(const GemvParams& prm0, int grid, bool pdl, cudaStream_t
     const int scratch = prm.rht_block > 256 ? PX::NWARP * 256 * 4 : 0;
     const int rounds = spb >= 1 && spb <= PX::NWARP ? (prm.batch * (prm.d_in / prm.rht_block) + PX::NWARP / spb - 1) /
                                                           (PX::NWARP / spb) : 1 << 20;
-    if (rounds > kMaxRotRounds || xs_bytes + scratch + PX::NWARP * PX::STAGE > PX::AVAIL) return cudaErrorNotSupported;
+    if (rounds > fused_rht_max_rounds() || xs_bytes + scratch + PX::NWARP * PX::STAGE > PX::AVAIL) return cudaErrorNotSupported;
     prm.xs_bytes = xs_bytes + scratch;
     prm.xs_rs = rs;
     prm.ns = (std::min)(4, (PX::AVAIL - prm.xs_bytes) / (PX::NWARP * PX::STAGE));

@@ -78,11 +78,11 @@ bool pdl_disabled_by_env() {
   return off;
 }
 
-bool fused_rht_disabled_by_env() {   // QP_FUSED_RHT=0: always launch the separate rotation kernel
+bool fused_rht_by_env() {   // QP_FUSED_RHT=1: QP_FUSE_RHT on every forward (experiments)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("QP_FUSED_RHT");
-    v = (e && atoi(e) == 0) ? 1 : 0;
+    v = (e && atoi(e) != 0) ? 1 : 0;
   }
   return v == 1;
 }
@@ -354,8 +354,9 @@ struct FusedRot {
 
 qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, const int* rt_begin, void* const* ys,
                    const int* ldy, qp_dtype yt, bool pdl, cudaStream_t s, bool y_atomic, int side_ctas = 0,
-                   const FusedRot* fr = nullptr, bool* unsupported = nullptr) {
+                   const FusedRot* fr = nullptr, bool* unsupported = nullptr, bool y_accum = false) {
   GemvParams p{};
+  p.y_accum = y_accum ? 1 : 0;
   if (fr) {
     p.x_raw = fr->x;
     p.x_dtype = (int)fr->xt;
@@ -676,11 +677,12 @@ qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch
   const long long zn[1] = {(long long)batch * l->d_out};
   const int rtb[2] = {0, l->d_out / kTileRows};
   const int ldy[1] = {l->d_out};
-  if (!(flags & QP_X_PREROTATED) && !(flags & QP_SEPARATE_RHT) && !fused_rht_disabled_by_env()) {
-    // one kernel: every CTA rotates x itself (and zeroes y) -- no rotation kernel on the path
+  if (!(flags & QP_X_PREROTATED) && ((flags & QP_FUSE_RHT) || fused_rht_by_env())) {
+    // one kernel: every CTA rotates x itself (and zeroes y) -- no rotation kernel on the path;
+    // falls through to the two-kernel path when x' does not fit the fused plan
     const FusedRot fr{l->rht, x, xt, atomic && !(flags & QP_Y_ACCUMULATE)};
     bool unsup = false;
-    st = run_gemv(l, nullptr, batch, 1, rtb, ys, ldy, yt, pdl, s, atomic, 0, &fr, &unsup);
+    st = run_gemv(l, nullptr, batch, 1, rtb, ys, ldy, yt, pdl, s, atomic, 0, &fr, &unsup, (flags & QP_Y_ACCUMULATE) != 0);
     if (st != QP_OK || !unsup) return st;
   }
   int side = 0;
@@ -698,7 +700,8 @@ qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch
     cudaError_t e = launch_zero(zp, side, pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "zero kernel launch");
   }
-  return run_gemv(l, xr, batch, 1, rtb, ys, ldy, yt, pdl, s, atomic, side);
+  return run_gemv(l, xr, batch, 1, rtb, ys, ldy, yt, pdl, s, atomic, side, nullptr, nullptr,
+                  (flags & QP_Y_ACCUMULATE) != 0);
 }
 
 qp_status qp_dequantize(const qp_layer* l, void* W_hat_fp16, void* stream) {
@@ -790,10 +793,11 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
     rtb[i + 1] = rtb[i] + g->d_outs[i] / kTileRows;
     ldy[i] = g->d_outs[i];
   }
-  if (!(flags & QP_X_PREROTATED) && !(flags & QP_SEPARATE_RHT) && !fused_rht_disabled_by_env()) {
+  if (!(flags & QP_X_PREROTATED) && ((flags & QP_FUSE_RHT) || fused_rht_by_env())) {
     const FusedRot fr{l->rht, x, xt, atomic && !(flags & QP_Y_ACCUMULATE)};
     bool unsup = false;
-    st = run_gemv(l, nullptr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic, 0, &fr, &unsup);
+    st = run_gemv(l, nullptr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic, 0, &fr, &unsup,
+                  (flags & QP_Y_ACCUMULATE) != 0);
     if (st != QP_OK || !unsup) return st;
   }
   int side = 0;
@@ -813,7 +817,8 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
     cudaError_t e = launch_zero(zp, side, !(flags & QP_NO_PDL), s);
     if (e != cudaSuccess) return cuda_fail(e, "zero kernel launch");
   }
-  return run_gemv(l, xr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic, side);
+  return run_gemv(l, xr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic, side, nullptr, nullptr,
+                  (flags & QP_Y_ACCUMULATE) != 0);
 }
 
 qp_status qp_shard_range(int d_out, int d_in, qp_scheme scheme, int bits_x4, int rank, int world, int* row0,

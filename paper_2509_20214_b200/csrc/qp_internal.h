@@ -54,6 +54,7 @@ struct GemvParams {
   int ldy[kMaxGroup];          // leading dimension (elements) of y[i] rows (= d_out_i)
   int y_f32;                   // 1: fp32 output, 0: fp16 output
   int y_atomic;                // 1: y was zeroed; CTAs sharing a row tile red.add their scaled partials
+  int y_accum;                 // 1: QP_Y_ACCUMULATE -- row tiles owned by one warp add into y too
   uint32_t zero;               // always 0 (an operand the compiler cannot constant-fold)
   // shared-memory plan chosen at launch (qp_gemv.cuh launch_plan)
   int ns;                      // code-ring stages per warp (1..4)

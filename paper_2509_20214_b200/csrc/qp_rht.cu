@@ -192,6 +192,17 @@ cudaError_t launch_gather_permute(const void* src, void* dst, int world, int bat
   return cudaGetLastError();
 }
 
+int fused_rht_max_rounds() {
+  // in-CTA rotation rounds (each: an L2 round trip for x + the butterflies) above which the
+  // separate, PDL-overlapped rotation kernel is cheaper (profiles/r1/ab_xs_r1.md section 5)
+  static int n = -1;
+  if (n < 0) {
+    const char* e = getenv("QP_FUSED_RHT_ROUNDS");
+    n = e ? atoi(e) : 4;
+  }
+  return n;
+}
+
 int env_no_xs() {
   // x' staged in shared memory is opt-in (QP_XS=1): measured slower than the register path on
   // the C2 shapes (profiles/r1/ab_xs_r1.md)

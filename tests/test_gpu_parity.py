@@ -335,10 +335,10 @@ def test_y_accumulate_flag():
 ])
 @pytest.mark.parametrize("x_dtype", [torch.float16, torch.bfloat16, torch.float32])
 def test_fused_rotation_path(d_out, d_in, scheme, bits_x4, batch, x_dtype):
-    """Default qp_linear_fwd fuses the rotation into the GEMV kernel when x' fits its plan (one
-    launch; y zeroed in-kernel); QP_SEPARATE_RHT forces rotation kernel + GEMV. Both meet the
-    oracle bar and agree with each other (x' is bitwise the same; only the atomic summation order
-    of split row tiles differs)."""
+    """QP_FUSE_RHT fuses the rotation into the GEMV kernel when x' fits its plan (one launch; y
+    zeroed in-kernel); the default is rotation kernel + GEMV. Both meet the oracle bar and agree
+    with each other (x' is bitwise the same; only the atomic summation order of split row tiles
+    differs)."""
     Lb = _need_gpu()
     lay, codes, s, ocb = _layer(scheme, bits_x4, d_out, d_in, layer_id=21)
     x = activations_fp16(batch, d_in)
@@ -347,35 +347,37 @@ def test_fused_rotation_path(d_out, d_in, scheme, bits_x4, batch, x_dtype):
         xin = torch.from_numpy(x).to(x_dtype).float().numpy().astype(np.float64)
     y_ref = linear.linear_from_codes(codes, d_out, d_in, scheme, bits_x4, ocb, s, xin, SEED)
     n0 = Lb.launch_count()
-    y_f = _fwd(lay, x, batch, x_dtype=x_dtype)
+    y_f = _fwd(lay, x, batch, x_dtype=x_dtype, flags=Lb.QP_FUSE_RHT)
     n_fused = Lb.launch_count() - n0
     n0 = Lb.launch_count()
-    y_s = _fwd(lay, x, batch, x_dtype=x_dtype, flags=Lb.QP_SEPARATE_RHT)
+    y_s = _fwd(lay, x, batch, x_dtype=x_dtype)
     n_sep = Lb.launch_count() - n0
     assert n_sep == 2 and n_fused in (1, 2)
     for y in (y_f, y_s):
         assert np.max(linear.normwise_error(y, y_ref)) <= TOL
     assert np.max(np.abs(y_f - y_s)) <= 1e-5 * np.max(np.abs(y_s))
     # fp16 output (in-order reduction, no zeroing) and y accumulate through the fused path
-    y16 = _fwd(lay, x, batch, y_dtype=torch.float16, x_dtype=x_dtype)
+    y16 = _fwd(lay, x, batch, y_dtype=torch.float16, x_dtype=x_dtype, flags=Lb.QP_FUSE_RHT)
     assert np.max(linear.normwise_error(y16, y_ref)) <= TOL
     xt = torch.from_numpy(x).to("cuda", x_dtype)
-    y = torch.full((batch, d_out), 0.25, device="cuda")
-    lay.forward(xt, batch, y, flags=Lb.QP_Y_ACCUMULATE)
-    lay.forward(xt, batch, y, flags=Lb.QP_Y_ACCUMULATE)
-    torch.cuda.synchronize()
-    assert np.max(linear.normwise_error(y.cpu().numpy() - 0.25, 2 * y_ref)) <= TOL
+    for fl in (Lb.QP_FUSE_RHT, 0):          # (owned row tiles too: 64x256 has one tile per row tile)
+        y = torch.full((batch, d_out), 0.25, device="cuda")
+        lay.forward(xt, batch, y, flags=fl | Lb.QP_Y_ACCUMULATE)
+        lay.forward(xt, batch, y, flags=fl | Lb.QP_Y_ACCUMULATE)
+        torch.cuda.synchronize()
+        assert np.max(linear.normwise_error(y.cpu().numpy() - 0.25, 2 * y_ref)) <= TOL
 
 
 def test_fused_rotation_is_single_kernel_at_batch1():
-    """The C2 shapes at batch 1 take the one-kernel path (the bench's step)."""
+    """With QP_FUSE_RHT the C2 shapes at batch 1 take the one-kernel path; without it, two."""
     Lb = _need_gpu()
     for d_out, d_in in ((4096, 4096), (1024, 14336)):
         lay, _, _, _ = _layer("tcq", 10, d_out, d_in, layer_id=22)
         x = activations_fp16(1, d_in)
-        n0 = Lb.launch_count()
-        _fwd(lay, x, 1)
-        assert Lb.launch_count() - n0 == 1
+        for fl, n in ((Lb.QP_FUSE_RHT, 1), (0, 2)):
+            n0 = Lb.launch_count()
+            _fwd(lay, x, 1, flags=fl)
+            assert Lb.launch_count() - n0 == n
 
 
 def test_fused_rotation_repeated_launches_in_graph():
@@ -388,12 +390,12 @@ def test_fused_rotation_repeated_launches_in_graph():
     y = torch.empty(1, 2048, device="cuda")
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
-        lay.forward(x, 1, y, stream=st)
+        lay.forward(x, 1, y, flags=Lb.QP_FUSE_RHT, stream=st)
         st.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=st):
             for _ in range(16):
-                lay.forward(x, 1, y, stream=st)
+                lay.forward(x, 1, y, flags=Lb.QP_FUSE_RHT, stream=st)
         for _ in range(4):
             g.replay()
         st.synchronize()
