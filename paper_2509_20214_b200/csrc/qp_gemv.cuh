@@ -135,23 +135,27 @@ template <int MODE, int C, int L, int TB, int REPS>
 struct Dec {
   static constexpr int NW = 4 * C;
   static constexpr int PB = RepBits<REPS>::value;   // log2(REPS * 4): key -> byte offset shift
+  // key shift of the TCQ modes: the (sign, idx) key sits at bits [L-1-TB, L-1] of p and must land
+  // at bit PB of the table byte offset
+  static constexpr int KSH = PB - (L - 1 - TB);
   template <int J>
-  __device__ __forceinline__ static uint32_t step(const uint32_t* w, uint32_t laneoff) {
+  __device__ __forceinline__ static uint32_t step(const uint32_t* w, uint32_t laneoff, uint32_t mulk) {
     if constexpr (MODE == DEC_TCQ_PRESIGNED) {
       // window int(r[J*s : J*s+L]) -> p = (w+1) w mod 2^L -> key = bits
-      // [L-1-TB, L-1] of p (sign bit on top) -> pre-signed entry
+      // [L-1-TB, L-1] of p (sign bit on top) -> pre-signed entry.
+      // The key shift is a multiply by mulk = 2^KSH held in a register (a runtime value to ptxas),
+      // so it issues as a second IMAD on the FMA pipe instead of an IADD3/SHF on the ALU pipe,
+      // which the window funnel shift and the mask already load (2 ALU + 2 FMA ops per pair).
       const uint32_t win = field<J * C, L, 0, NW>(w);
       const uint32_t p = win * win + win;
-      constexpr int SH = PB - (L - 1 - TB);
       constexpr uint32_t MASK = ((1u << (TB + 1)) - 1u) << PB;
-      const uint32_t k = SH >= 0 ? (p << (SH >= 0 ? SH : 0)) : (p >> (SH < 0 ? -SH : 0));
+      const uint32_t k = KSH >= 0 ? p * mulk : (p >> (KSH < 0 ? -KSH : 0));
       return lds32(and_or<MASK>(k, laneoff));
     } else if constexpr (MODE == DEC_TCQ_UNSIGNED) {
       const uint32_t win = field<J * C, L, 0, NW>(w);
       const uint32_t p = win * win + win;
-      constexpr int SH = PB - (L - 1 - TB);
       constexpr uint32_t MASK = ((1u << TB) - 1u) << PB;
-      const uint32_t k = SH >= 0 ? (p << (SH >= 0 ? SH : 0)) : (p >> (SH < 0 ? -SH : 0));
+      const uint32_t k = KSH >= 0 ? p * mulk : (p >> (KSH < 0 ? -KSH : 0));
       const uint32_t v = lds32(((k & MASK) | laneoff));
       return v ^ ((p << (16 - L)) & 0x8000u);             // sflp on the first coordinate
     } else if constexpr (MODE == DEC_LUT2) {
@@ -176,11 +180,21 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ void load_x8(uint32_t* dst, const __half* src) {   // 8 regs = 16 halves
+// 8 regs = 16 halves = one full 32-byte sector per lane: a single 256-bit load on sm_100
+// (LDG.E.ENL2.256); two 128-bit loads would each touch 32 half-used sectors per warp at batch 8
+// (8 rows x 4 column groups), doubling the L1 tag / sector work that throttles the MIO queue.
+__device__ __forceinline__ void load_x8(uint32_t* dst, const __half* src) {
+#ifdef QP_X_LDG128
   const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(src));
   const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
   dst[0] = v0.x; dst[1] = v0.y; dst[2] = v0.z; dst[3] = v0.w;
   dst[4] = v1.x; dst[5] = v1.y; dst[6] = v1.z; dst[7] = v1.w;
+#else
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(dst[0]), "=r"(dst[1]), "=r"(dst[2]), "=r"(dst[3]), "=r"(dst[4]), "=r"(dst[5]), "=r"(dst[6]),
+                 "=r"(dst[7])
+               : "l"(src));
+#endif
 }
 
 // Decode one tile's 128 steps of this lane and multiply-accumulate (GEMV) or store (dequant).
@@ -201,7 +215,8 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
 }
 
 template <int MODE, int C, int L, int TB, int REPS, bool DEQ, bool XS>
-__device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, uint32_t* xb, float (&acc)[2 * kAccSets][4],
+__device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, uint32_t mulk, uint32_t* xb,
+                                          float (&acc)[2 * kAccSets][4],
                                           uint32_t* wout_lane, int ldw_words, const __half* x_hi,
                                           const __half* x_next, uint32_t xs_addr) {
   using D = Dec<MODE, C, L, TB, REPS>;
@@ -221,10 +236,10 @@ __device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, u
     static_for<2>([&](auto M) {
       constexpr int m = decltype(M)::value;
       constexpr int j = 8 * kap + 4 * m;
-      const uint32_t a0 = D::template step<j + 0>(w, laneoff);
-      const uint32_t a1 = D::template step<j + 1>(w, laneoff);
-      const uint32_t a2 = D::template step<j + 2>(w, laneoff);
-      const uint32_t a3 = D::template step<j + 3>(w, laneoff);
+      const uint32_t a0 = D::template step<j + 0>(w, laneoff, mulk);
+      const uint32_t a1 = D::template step<j + 1>(w, laneoff, mulk);
+      const uint32_t a2 = D::template step<j + 2>(w, laneoff, mulk);
+      const uint32_t a3 = D::template step<j + 3>(w, laneoff, mulk);
       if constexpr (DEQ) {
         // step -> (row, col): row = 16m + g + 8(rho&1), col = 64q + 4kap + 2(rho>>1)
         uint32_t* p = wout_lane + (16 * m) * ldw_words + 2 * kap;
@@ -547,6 +562,12 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
     if (lane == 0 && a + st < b) fetch(f_ptr, tile_bytes(kt_f), st);
     advance_f();
   }
+#ifdef QP_EARLY_TRIGGER
+  // (experiment) let the next kernel launch now so its CTAs take SMs as this grid's CTAs exit:
+  // same GEMV-alone time, 12% slower C2 step (the next rotation kernel's CTAs then queue behind
+  // the GEMV CTAs; profiles/r1/ab_xs_r1.md section 8)
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
   asm volatile("griddepcontrol.wait;" ::: "memory");
   stamp(5);
   // this lane's x' row in the staged copy (lanes without a batch row read row batch-1: their
@@ -597,6 +618,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
 
   stamp(1);
   const uint32_t laneoff = (uint32_t)(lane % REPS) * 4u;
+  const uint32_t mulk = (1u << (Dec<MODE, CLO, L, TB, REPS>::KSH > 0 ? Dec<MODE, CLO, L, TB, REPS>::KSH : 0)) + p.zero;
   float acc[2 * kAccSets][4];
 #pragma unroll
   for (int m = 0; m < 2 * kAccSets; ++m)
@@ -643,9 +665,9 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
     }
     const uint32_t xs_addr = xs_lane + (uint32_t)(kt * 4 * 136);
     if (CLO == CHI || kt < KH)
-      tile_body<MODE, CLO, L, TB, REPS, DEQ, XS>(cur, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next, xs_addr);
+      tile_body<MODE, CLO, L, TB, REPS, DEQ, XS>(cur, laneoff, mulk, xb, acc, wout_lane, ldw, x_hi, x_next, xs_addr);
     else
-      tile_body<MODE, CHI, L, TB, REPS, DEQ, XS>(cur, laneoff, xb, acc, wout_lane, ldw, x_hi, x_next, xs_addr);
+      tile_body<MODE, CHI, L, TB, REPS, DEQ, XS>(cur, laneoff, mulk, xb, acc, wout_lane, ldw, x_hi, x_next, xs_addr);
     if (++st == NS) { st = 0; par ^= 1u; }
 
     if constexpr (!DEQ) {
@@ -718,7 +740,10 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
     kt = kt_n; rt = rt_n;
   }
   stamp(2);
+#ifndef QP_EARLY_TRIGGER
+  // dependents (the next layer's rotation + GEMV) launch once every CTA is past its main loop
   asm volatile("griddepcontrol.launch_dependents;");
+#endif
   if (DEQ || nC <= 0 || p.y_atomic) {
     flush_stamps(3);
     return;

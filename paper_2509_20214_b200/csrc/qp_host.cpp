@@ -435,6 +435,9 @@ qp_status check_fwd_args(const void* x, qp_dtype xt, int batch, qp_dtype yt, uns
     return fail(QP_ERR_INVALID_ARG, "dtype: x in {F16,BF16,F32}, y in {F16,F32}");
   if ((flags & QP_X_PREROTATED) && xt != QP_F16)
     return fail(QP_ERR_INVALID_ARG, "QP_X_PREROTATED requires fp16 x (the output dtype of qp_rht_apply)");
+  if ((flags & QP_X_PREROTATED) && (reinterpret_cast<uintptr_t>(x) & 31u))
+    return fail(QP_ERR_INVALID_ARG, "QP_X_PREROTATED x must be 32-byte aligned (the GEMV reads it with 256-bit "
+                "loads). Remedy: pass the start of a device allocation");
   if ((flags & QP_Y_ACCUMULATE) && (yt != QP_F32 || (flags & QP_DETERMINISTIC)))
     return fail(QP_ERR_INVALID_ARG, "QP_Y_ACCUMULATE needs fp32 y and excludes QP_DETERMINISTIC");
   return QP_OK;

@@ -1,7 +1,7 @@
 # One gpurun session producing the round's GPU evidence (outputs in gpurun_out/):
 # GPU parity tests, smoke, bench line (+ reference arm), per-launch DRAM traffic of the GEMV (ncu),
 # ncu launch list of the bench step, ncu --set full of the dominant kernel, the C3 palette sweep
-# and the C5 decoder layer.
+# the C5 decoder layer and the C4 70B row shards (compute side, one GPU).
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/ev_gpu.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ev_pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/ev_pytest_gpu.txt
@@ -18,4 +18,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:qp_g
   -o gpurun_out/ev_prof_gemv python tools/prof_gemv.py --shape 14336x4096 --scheme tcq --bits-x4 10 --iters 8 > gpurun_out/ev_ncu_full.log 2>&1
 timeout 1500 python tools/sweep.py --batches 1,2,4,8 --out gpurun_out/ev_sweep.jsonl > gpurun_out/ev_sweep.txt 2>&1
 timeout 600 python tools/decoder_layer.py --out gpurun_out/ev_c5.jsonl > gpurun_out/ev_c5.txt 2>&1
+timeout 900 python tools/sweep.py --shapes 28672x8192,8192x28672 --widths c4 --batches 1,8 --shards 1,2,4,8 \
+  --out gpurun_out/ev_c4.jsonl > gpurun_out/ev_c4.txt 2>&1
 exit 0

@@ -13,6 +13,7 @@ PALETTE = ([("tcq", x) for x in range(6, 21, 2)] + [("half_tcq", x) for x in ran
            + [("vq", x) for x in range(6, 25, 2)] + [("nuq", x) for x in range(8, 33, 4)]
            + [("unif", x) for x in range(8, 33, 4)])
 TARGET = [(s, x) for s, x in PALETTE if 8 <= x <= 18]       # north star: 2 .. 4.5 bits
+C4 = [("tcq", 10), ("half_tcq", 13), ("tcq", 16), ("vq", 12), ("nuq", 16)]
 
 
 def tlut_bits(scheme: str, bits_x4: int) -> int:

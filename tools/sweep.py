@@ -2,7 +2,12 @@
 us/launch and achieved GB/s on algorithmic bytes for every (scheme, width, shape, batch).
 
     python tools/sweep.py [--shapes 4096x4096,14336x4096,4096x14336] [--batches 1,2,4,8]
-                          [--widths target|all] [--out gpurun_out/sweep.jsonl]
+                          [--widths target|all] [--shards 1,2,4,8] [--out gpurun_out/sweep.jsonl]
+
+--shards P1,...: C4 (BASELINE.json configs[3]) on one GPU: each point is the rank-0 row shard of
+the layer at world size P (d_out/P contiguous rows = a byte slice of the codes, DESIGN.md section
+7), timed alone; "job_gbs" = P x shard bytes / shard time, i.e. the compute side of the row-sharded
+layer with every rank equally fast. The NCCL all-gather is not included (one GPU per gpurun call).
 
 Each point: R replicas of the layer (together > 2x L2, so every launch streams from HBM), one
 CUDA graph of 4R back-to-back launches (pre-rotated x, fp32 y with QP_Y_ACCUMULATE: exactly one
@@ -78,15 +83,17 @@ def main():
     ap.add_argument("--batches", default="1,2,4,8")
     ap.add_argument("--widths", default="target")
     ap.add_argument("--schemes", default="")
+    ap.add_argument("--shards", default="1")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
     a = ap.parse_args()
     peak, _ = P.hbm_peak()
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
-    widths = P.TARGET if a.widths == "target" else P.PALETTE
+    widths = {"target": P.TARGET, "c4": P.C4}.get(a.widths, P.PALETTE)
     if a.schemes:
         widths = [w for w in widths if w[0] in a.schemes.split(",")]
     shapes = [tuple(map(int, s.split("x"))) for s in a.shapes.split(",")]
     batches = [int(b) for b in a.batches.split(",")]
+    shards = [int(w) for w in a.shards.split(",")]
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     cbs, rots = {}, {}
     t0 = time.time()
@@ -94,11 +101,15 @@ def main():
         for (d_out, d_in) in shapes:
             for scheme, x4 in widths:
                 for batch in batches:
-                    r = point(scheme, x4, d_out, d_in, batch, cbs, rots, l2, peak)
-                    f.write(json.dumps(r) + "\n")
-                    f.flush()
-                    print(f'{d_out}x{d_in} {scheme:8s} {x4 / 4:5.2f}b B={batch}: {r["us"]:8.2f} us  '
-                          f'{r["gbs"]:7.1f} GB/s  {100 * r["frac"]:5.1f}%', flush=True)
+                    for world in shards:
+                        r = point(scheme, x4, d_out // world, d_in, batch, cbs, rots, l2, peak)
+                        if world > 1 or len(shards) > 1:
+                            r.update(world=world, full_d_out=d_out, job_gbs=round(world * r["gbs"], 1),
+                                     job_frac_per_gpu=r["frac"], note="rank-0 shard alone, all-gather excluded")
+                        f.write(json.dumps(r) + "\n")
+                        f.flush()
+                        print(f'{d_out}x{d_in} P={world} {scheme:8s} {x4 / 4:5.2f}b B={batch}: {r["us"]:8.2f} us  '
+                              f'{r["gbs"]:7.1f} GB/s  {100 * r["frac"]:5.1f}%', flush=True)
     print(f"sweep done in {time.time() - t0:.0f} s")
 
 
