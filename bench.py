@@ -249,9 +249,33 @@ def main():
             lay = full.shard(rank, world) if world > 1 else full
             if world > 1:
                 del full
-            x = torch.from_numpy(activations_fp16(batch, d_in)).to(dev)
-            y = torch.empty(batch, d_out, dtype=torch.float32, device=dev)
-            insts.append(dict(layer=lay, x=x, y=y, meta=L))
+            insts.append(dict(layer=lay, meta=L))
+    # activations / outputs of a step live in one device buffer each (per replica), so the
+    # end-to-end measurement moves a step's inputs and results with one copy each way; every
+    # layer's x / y is a 256-byte-aligned view into them
+    def carve(buf, sizes, elem):
+        views, off = [], 0
+        for n in sizes:
+            views.append(buf[off:off + n])
+            off += -(-n * elem // 256) * 256 // elem
+        return views, off
+    n_layers = len(layers)
+    xs_sizes = [batch * L["d_in"] for L in layers]
+    ys_sizes = [batch * L["d_out"] for L in layers]
+    x_elems = carve(torch.empty(0), xs_sizes, 2)[1]
+    y_elems = carve(torch.empty(0), ys_sizes, 4)[1]
+    bufs = []
+    for rep in range(REPLICAS):
+        xb = torch.empty(x_elems, dtype=torch.float16, device=dev)
+        yb = torch.empty(y_elems, dtype=torch.float32, device=dev)
+        xv, _ = carve(xb, xs_sizes, 2)
+        yv, _ = carve(yb, ys_sizes, 4)
+        for j, L in enumerate(layers):
+            inst = insts[rep * n_layers + j]
+            inst["x"] = xv[j].view(batch, L["d_in"])
+            inst["x"].copy_(torch.from_numpy(activations_fp16(batch, L["d_in"])))
+            inst["y"] = yv[j].view(batch, L["d_out"])
+        bufs.append((xb, yb))
     torch.cuda.synchronize()
 
     def fwd(inst, stream=None, flags=0):
@@ -264,7 +288,6 @@ def main():
     # (QP_BENCH_EAGER=1 replays the step eagerly instead: ncu cannot profile our kernels inside
     #  captured graphs, so the launch-list profile in profiles/ is taken that way.)
     stream = torch.cuda.Stream(device=dev)
-    n_layers = len(layers)
     graphs = []
     eager = os.environ.get("QP_BENCH_EAGER") == "1"
 
@@ -343,25 +366,36 @@ def main():
     kflags = QL.QP_X_PREROTATED | QL.QP_Y_ACCUMULATE
     torch.cuda.synchronize()
     per_layer_us, gemv_time_s, gemv_alg = {}, 0.0, 0
-    n_rep = 8
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     for li, L in enumerate(layers):
+        # enough distinct copies of the layer that one graph's launches stream > 2x L2 of codes
+        # (every launch reads its codes from HBM), as tools/sweep.py does
         group = [insts[rep * n_layers + li] for rep in range(REPLICAS)]
+        nb = code_bytes(L["m"], L["d_in"], L["bits_x4"])
+        n_copies = max(REPLICAS, -(-2 * l2 // nb) + 1)
+        while len(group) < n_copies:
+            src = group[len(group) % REPLICAS]["layer"]
+            group.append(dict(layer=QL.Layer.from_codes(random_code_bytes(nb, 7000 + 97 * li + len(group)),
+                                                        channel_scales(L["d_out"], L["d_in"])[:L["m"]], L["m"],
+                                                        L["d_in"], L["scheme"], L["bits_x4"],
+                                                        cbs[(L["scheme"], L["bits_x4"])], rots[L["d_in"]])))
+        n_rep = 2 * len(group)
         with torch.cuda.stream(stream):
             for inst in group:
                 inst["layer"].forward(xr[L["d_in"]], batch, yacc[L["d_out"]], flags=kflags, stream=stream)
             stream.synchronize()
             if eager:
-                def g_replay(group=group, L=L):
+                def g_replay(group=group, L=L, n_rep=n_rep):
                     for k in range(n_rep):
-                        group[k % REPLICAS]["layer"].forward(xr[L["d_in"]], batch, yacc[L["d_out"]],
+                        group[k % len(group)]["layer"].forward(xr[L["d_in"]], batch, yacc[L["d_out"]],
                                                              flags=kflags, stream=stream)
                 g = type("G", (), {"replay": staticmethod(g_replay)})
             else:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
                     for k in range(n_rep):
-                        group[k % REPLICAS]["layer"].forward(xr[L["d_in"]], batch, yacc[L["d_out"]],
-                                                             flags=kflags, stream=stream)
+                        group[k % len(group)]["layer"].forward(xr[L["d_in"]], batch, yacc[L["d_out"]],
+                                                               flags=kflags, stream=stream)
             for _ in range(3):
                 g.replay()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -381,31 +415,56 @@ def main():
     traffic, traffic_src = ncu_traffic(layers, batch)
 
     # ---- end to end through the public API with host buffers (N=1 only) ------------------
+    # Every step: one H2D copy of the step's 9 activation vectors from pinned host memory, the 9
+    # qp_linear_fwd calls, one D2H copy of the 9 results into pinned host memory -- captured with
+    # the forwards in a CUDA graph per replica (as a serving loop would), timed with events.
     e2e = None
     if world == 1:
-        hx = [torch.from_numpy(activations_fp16(batch, L["d_in"])).pin_memory() for L in layers]
-        hy = [torch.empty(batch, L["d_out"], dtype=torch.float32).pin_memory() for L in layers]
-        h2d = sum(t.numel() * 2 for t in hx)
-        d2h = sum(t.numel() * 4 for t in hy)
+        hx = torch.empty(x_elems, dtype=torch.float16).pin_memory()
+        hy = torch.empty(y_elems, dtype=torch.float32).pin_memory()
+        hx.copy_(bufs[0][0].cpu())
+        h2d = hx.numel() * 2
+        d2h = hy.numel() * 4
+        e2e_graphs = []
         with torch.cuda.stream(stream):
             def e2e_step(rep):
-                for j, inst in enumerate(insts[rep * n_layers:(rep + 1) * n_layers]):
-                    inst["x"].copy_(hx[j], non_blocking=True)
+                bufs[rep][0].copy_(hx, non_blocking=True)
+                for inst in insts[rep * n_layers:(rep + 1) * n_layers]:
                     fwd(inst, stream)
-                    hy[j].copy_(inst["y"], non_blocking=True)
-            for i in range(args.warmup):
-                e2e_step(i % REPLICAS)
+                hy.copy_(bufs[rep][1], non_blocking=True)
+            for rep in range(REPLICAS):
+                e2e_step(rep)
             stream.synchronize()
-            t0 = time.perf_counter()
+            for rep in range(REPLICAS):
+                if eager:
+                    e2e_graphs.append(None)
+                    continue
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    e2e_step(rep)
+                e2e_graphs.append(g)
+
+            def run(i):
+                g = e2e_graphs[i % REPLICAS]
+                if g is None:
+                    e2e_step(i % REPLICAS)
+                else:
+                    g.replay()
+            for i in range(args.warmup):
+                run(i)
+            stream.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for i in range(args.steps):
-                e2e_step(i % REPLICAS)
+                run(i)
             e1.record(stream)
             e1.synchronize()
         e2e_ms = e0.elapsed_time(e1) / args.steps
+        assert torch.isfinite(hy).all(), "non-finite y read back"
         e2e = {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4)}
+               "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4),
+               "method": "per step: 1 H2D copy of all activations (pinned), the 9 qp_linear_fwd calls, 1 D2H copy of "
+                         "all outputs (pinned); CUDA graph per replica; events on the stream"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -436,7 +495,8 @@ def main():
                          "traffic": round(traffic) if traffic else None, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": round(gemv_alg / n_layers),
                          "kernel": "qp_gemv_kernel (fused dequant-GEMV), all 9 layers, CUDA graph of back-to-back "
-                                   "launches per layer, events on the launching stream",
+                                   "launches per layer cycling > 2x L2 of distinct layer copies (codes stream from "
+                                   "HBM), events on the launching stream",
                          "peak_kind": peak_kind, "avg_launch_us": round(gemv_avg_ms * 1e3, 3)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches_per_step * args.steps),
             "clocks": ck,

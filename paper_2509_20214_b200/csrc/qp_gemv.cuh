@@ -203,11 +203,6 @@ __device__ __forceinline__ void load_x8(uint32_t* dst, const __half* src) {
 // (x_next) once kappa 0..7 are done, so activation loads never sit on the critical path and
 // need no extra registers. Lanes with no batch row (x_hi == nullptr) keep zeros (loading a valid
 // row for them instead measured 10-25% slower: profiles/r1/ab_xs_r1.md section 4).
-#ifdef QP_ACC4
-constexpr int kAccSets = 2;   // independent accumulator chains per row block (k-step parity)
-#else
-constexpr int kAccSets = 1;
-#endif
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
@@ -216,7 +211,7 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
 
 template <int MODE, int C, int L, int TB, int REPS, bool DEQ, bool XS>
 __device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, uint32_t mulk, uint32_t* xb,
-                                          float (&acc)[2 * kAccSets][4],
+                                          float (&acc)[2][4],
                                           uint32_t* wout_lane, int ldw_words, const __half* x_hi,
                                           const __half* x_next, uint32_t xs_addr) {
   using D = Dec<MODE, C, L, TB, REPS>;
@@ -254,9 +249,9 @@ __device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, u
           xb[2 * ((kap + 1) & 1)] = bx.x;
           xb[2 * ((kap + 1) & 1) + 1] = bx.y;
         }
-        mma16816(acc[m + 2 * (kap % kAccSets)], a0, a1, a2, a3, xb[2 * (kap & 1)], xb[2 * (kap & 1) + 1]);
+        mma16816(acc[m], a0, a1, a2, a3, xb[2 * (kap & 1)], xb[2 * (kap & 1) + 1]);
       } else {
-        mma16816(acc[m + 2 * (kap % kAccSets)], a0, a1, a2, a3, xb[2 * kap], xb[2 * kap + 1]);
+        mma16816(acc[m], a0, a1, a2, a3, xb[2 * kap], xb[2 * kap + 1]);
       }
     });
     if constexpr (!DEQ && !XS && kap == 7) {
@@ -459,12 +454,17 @@ __device__ __forceinline__ void rotate_x(const GemvParams& p, uint8_t* xs, float
 
 // XM: 0 = x' B fragments from global into registers, 1 = x' staged in shared memory,
 //     2 = x' computed in shared memory by every CTA from raw x (fused rotation) + in-kernel zeroing
-template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, int XM>
+// RP: row tiles per work unit. RP = 2 (batch >= 2, fp32 atomic output): a warp decodes the two
+// row tiles of a row pair at the same k tile back to back with the same x' B fragments, halving
+// the activation loads per weight.
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, int XM, int RP>
 __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWARP * 32, 1)
     qp_gemv_kernel(const __grid_constant__ GemvParams p) {
   constexpr bool XS = XM != 0;
   using PL = Plan<MODE, CLO, CHI, TB, REPS, XS>;
   constexpr int CMAX = PL::CMAX, NWARP = PL::NWARP;
+  static_assert(RP == 1 || (RP == 2 && !DEQ), "row pairs are a GEMV-only (atomic epilogue) variant");
+  constexpr int USTAGE = RP * PL::STAGE;          // ring stage: one work unit
   const int NS = p.ns;
   uint8_t* smem = qp_smem;
   uint8_t* tab = smem;
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
   tb.load(p.table);
   const int g = lane >> 2, q = lane & 3;
   // tile indices are 32-bit: the host guarantees RT*KT*gridDim < 2^32
-  const uint32_t N = (uint32_t)p.RT * (uint32_t)p.KT;
+  const uint32_t N = (uint32_t)(p.RT / RP) * (uint32_t)p.KT;   // work units (row tile groups x k tiles)
   const uint32_t KT = p.KT;
   // host-computed reciprocals (qp_host.cpp div_magic): no 32-bit integer divisions in the prologue
   auto div_kt = [&](uint32_t x) -> uint32_t { return p.kt_magic ? __umulhi(x, p.kt_magic) : x / KT; };
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
   const long long rowtile_bytes = (long long)KH * 512 * CLO + (long long)(KT - KH) * 512 * CHI;
 
   // ---- this warp's code ring: NS stages, one tile each, filled by bulk async copies ----
-  const uint32_t ring = smem_u32(smem + PL::XS_OFF + p.xs_bytes) + (uint32_t)(warp * NS * PL::STAGE);
+  const uint32_t ring = smem_u32(smem + PL::XS_OFF + p.xs_bytes) + (uint32_t)(warp * NS * USTAGE);
   const uint32_t bars = smem_u32(smem + PL::BAR_OFF) + (uint32_t)(warp * NS * 8);
   uint64_t pol = 0;
   // bytes of k tile kt_ (half-TCQ: c_lo on the first KT/2 k tiles, c_hi on the rest)
@@ -511,19 +511,24 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
   // issue the copy of the tile at `src` into stage st (lane 0 only)
   auto fetch = [&](const uint8_t* src, uint32_t nbytes, int st, uint32_t dep = 0u) {
     const uint32_t bar = bars + 8u * st;
-    mbar_expect_tx(bar, nbytes);
-    bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, src, nbytes, bar, pol);
+    mbar_expect_tx(bar, nbytes * RP);
+#pragma unroll
+    for (int h = 0; h < RP; ++h)   // row tile h of the unit: the next row tile, same k tile
+      bulk_g2s(ring + (uint32_t)(st * USTAGE + h * PL::STAGE) + dep, src + h * rowtile_bytes, nbytes, bar, pol);
   };
-  uint32_t rt = div_kt(a);
+  uint32_t rt = div_kt(a);                         // row tile group (RP row tiles)
   int kt = (int)(a - rt * KT);
   // the refill cursor: the next tile to be fetched (its address advances by whole tiles: the
   // LAYOUT.md stream is row-tile-major, tiles of a row tile in k order, all contiguous)
-  const uint8_t* f_ptr = p.codes + (long long)rt * rowtile_bytes +
+  const uint8_t* f_ptr = p.codes + (long long)(RP * rt) * rowtile_bytes +
                          (kt < KH ? (long long)kt * 512 * CLO : (long long)KH * 512 * CLO + (long long)(kt - KH) * 512 * CHI);
   int kt_f = kt;
   auto advance_f = [&]() {
     f_ptr += tile_bytes(kt_f);
-    if (++kt_f == (int)KT) kt_f = 0;
+    if (++kt_f == (int)KT) {
+      kt_f = 0;
+      f_ptr += (RP - 1) * rowtile_bytes;             // skip the group's other row tiles
+    }
   };
   if (lane == 0) {
 #pragma unroll
@@ -538,11 +543,11 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
 
   // per-row scales of the current row tile, rows g, g+8, g+16, g+24 (prefetched into registers
   // when a row tile starts; consumed when its partial is flushed)
-  float sc[4];
-  auto load_scales = [&](uint32_t rt_) {
+  float sc[4 * RP];
+  auto load_scales = [&](uint32_t rt_) {             // rt_: row tile group
     if constexpr (!DEQ) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) sc[i] = __ldg(p.scales + rt_ * kTileRows + g + 8 * i);
+      for (int i = 0; i < 4 * RP; ++i) sc[i] = __ldg(p.scales + (RP * rt_ + (i >> 2)) * kTileRows + g + 8 * (i & 3));
     }
   };
   if (a < b) load_scales(rt);
@@ -619,9 +624,9 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
   stamp(1);
   const uint32_t laneoff = (uint32_t)(lane % REPS) * 4u;
   const uint32_t mulk = (1u << (Dec<MODE, CLO, L, TB, REPS>::KSH > 0 ? Dec<MODE, CLO, L, TB, REPS>::KSH : 0)) + p.zero;
-  float acc[2 * kAccSets][4];
+  float acc[2 * RP][4];                            // [row tile of the group][m]
 #pragma unroll
-  for (int m = 0; m < 2 * kAccSets; ++m)
+  for (int m = 0; m < 2 * RP; ++m)
 #pragma unroll
     for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
   const uint32_t a_rt = rt;
@@ -632,11 +637,17 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
   int st = 0;
   uint32_t par = 0;
   for (uint32_t t = a; t < b; ++t) {
-    // ---- this tile's stream words: stage st -> registers (c conflict-free 128-bit loads) ----
+    // ---- the unit's stream words: stage st -> registers (c conflict-free 128-bit loads per row
+    //      tile), then the row tile's decode + MAC; with RP = 2 the second row tile's words are
+    //      read after the first is decoded (same registers) and reuse its x' B fragments ----
     mbar_wait(bars + 8u * st, par);
-    {
-      const int c = (CLO == CHI || kt < KH) ? CLO : CHI;
-      const uint32_t src = ring + (uint32_t)(st * PL::STAGE) + (uint32_t)lane * 16u;
+    int kt_n = kt + 1;
+    uint32_t rt_n = rt;
+    if (kt_n == (int)KT) { kt_n = 0; ++rt_n; }
+    const int c = (CLO == CHI || kt < KH) ? CLO : CHI;
+#pragma unroll
+    for (int h = 0; h < RP; ++h) {
+      const uint32_t src = ring + (uint32_t)(st * USTAGE + h * PL::STAGE) + (uint32_t)lane * 16u;
 #pragma unroll
       for (int i = 0; i < CMAX; ++i) {
         if (CLO == CHI || i < c) {
@@ -644,30 +655,30 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
           cur[4 * i] = v.x; cur[4 * i + 1] = v.y; cur[4 * i + 2] = v.z; cur[4 * i + 3] = v.w;
         }
       }
-      // The stage is free once every lane's shared loads have returned: a warp reduction over the
-      // last loaded word of each lane (in-order shared pipeline: the earlier loads are done too)
-      // makes lane 0's refill depend on all of them (p.zero == 0 keeps the value unchanged).
-      const uint32_t last = (CLO == CHI || c == CMAX) ? cur[4 * CMAX - 1] : cur[4 * CLO - 1];
-      const uint32_t dep = __reduce_or_sync(0xffffffffu, last & p.zero);
-      if (lane == 0 && t + NS < b) fetch(f_ptr, tile_bytes(kt_f), st, dep);
-      advance_f();
+      if (h == RP - 1) {
+        // The stage is free once every lane's shared loads have returned: a warp reduction over
+        // the last loaded word of each lane (in-order shared pipeline: the earlier loads are done
+        // too) makes lane 0's refill depend on all of them (p.zero == 0 keeps the value unchanged).
+        const uint32_t last = (CLO == CHI || c == CMAX) ? cur[4 * CMAX - 1] : cur[4 * CLO - 1];
+        const uint32_t dep = __reduce_or_sync(0xffffffffu, last & p.zero);
+        if (lane == 0 && t + NS < b) fetch(f_ptr, tile_bytes(kt_f), st, dep);
+        advance_f();
+      }
+      const __half* x_hi = (!XS && xrow && h == 0) ? xlane + kt * kTileCols + 32 : nullptr;
+      const __half* x_next = (!XS && xrow && h == RP - 1 && t + 1 < b) ? xlane + kt_n * kTileCols : nullptr;
+      uint32_t* wout_lane = nullptr;
+      int ldw = 0;
+      if constexpr (DEQ) {
+        ldw = p.d_in / 2;
+        wout_lane = reinterpret_cast<uint32_t*>(p.w_out) + (size_t)(rt * kTileRows + g) * ldw + (kt * kTileCols + 64 * q) / 2;
+      }
+      const uint32_t xs_addr = xs_lane + (uint32_t)(kt * 4 * 136);
+      float (&acc_h)[2][4] = *reinterpret_cast<float(*)[2][4]>(&acc[2 * h][0]);
+      if (CLO == CHI || kt < KH)
+        tile_body<MODE, CLO, L, TB, REPS, DEQ, XS>(cur, laneoff, mulk, xb, acc_h, wout_lane, ldw, x_hi, x_next, xs_addr);
+      else
+        tile_body<MODE, CHI, L, TB, REPS, DEQ, XS>(cur, laneoff, mulk, xb, acc_h, wout_lane, ldw, x_hi, x_next, xs_addr);
     }
-    int kt_n = kt + 1;
-    uint32_t rt_n = rt;
-    if (kt_n == (int)KT) { kt_n = 0; ++rt_n; }
-    const __half* x_hi = (!XS && xrow) ? xlane + kt * kTileCols + 32 : nullptr;
-    const __half* x_next = (!XS && xrow && t + 1 < b) ? xlane + kt_n * kTileCols : nullptr;
-    uint32_t* wout_lane = nullptr;
-    int ldw = 0;
-    if constexpr (DEQ) {
-      ldw = p.d_in / 2;
-      wout_lane = reinterpret_cast<uint32_t*>(p.w_out) + (size_t)(rt * kTileRows + g) * ldw + (kt * kTileCols + 64 * q) / 2;
-    }
-    const uint32_t xs_addr = xs_lane + (uint32_t)(kt * 4 * 136);
-    if (CLO == CHI || kt < KH)
-      tile_body<MODE, CLO, L, TB, REPS, DEQ, XS>(cur, laneoff, mulk, xb, acc, wout_lane, ldw, x_hi, x_next, xs_addr);
-    else
-      tile_body<MODE, CHI, L, TB, REPS, DEQ, XS>(cur, laneoff, mulk, xb, acc, wout_lane, ldw, x_hi, x_next, xs_addr);
     if (++st == NS) { st = 0; par ^= 1u; }
 
     if constexpr (!DEQ) {
@@ -688,49 +699,49 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
             y_open = true;
           }
         }
-        if constexpr (kAccSets == 2) {
-#pragma unroll
-          for (int m = 0; m < 2; ++m)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) { acc[m][r] += acc[m + 2][r]; acc[m + 2][r] = 0.f; }
-        }
-        const uint32_t rs = rt * KT;
+        const uint32_t rs = rt * KT;                     // (in work units)
         const bool own = (a <= rs) && (b >= rs + KT);
-        if (own) {
 #pragma unroll
-          for (int m = 0; m < 2; ++m)
+        for (int h = 0; h < RP; ++h) {
+          const int rth = RP * (int)rt + h;             // row tile
+          if (own) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-              if (bb < p.batch) store_out(p, (int)rt, row, bb, acc[m][r], sc[2 * m + (r >> 1)]);
-            }
-        } else if (p.y_atomic) {
-          // y was zeroed by the preceding kernel: add this warp's scaled partial straight into it
-          // (fire-and-forget RED.ADD.F32; no shared-memory reduction, no barrier)
-          int i = 0;
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
+                if (bb < p.batch) store_out(p, rth, row, bb, acc[2 * h + m][r], sc[4 * h + 2 * m + (r >> 1)]);
+              }
+          } else if (RP == 2 || p.y_atomic) {
+            // y was zeroed by the preceding kernel: add this warp's scaled partial straight into it
+            // (fire-and-forget RED.ADD.F32; no shared-memory reduction, no barrier). RP = 2 is only
+            // launched for the atomic epilogue.
+            int i = 0;
 #pragma unroll 1
-          while (i + 1 < p.n_out && (int)rt >= p.rt_begin[i + 1]) ++i;
-          float* yb = reinterpret_cast<float*>(p.y[i]) + (rt - p.rt_begin[i]) * kTileRows;
+            while (i + 1 < p.n_out && rth >= p.rt_begin[i + 1]) ++i;
+            float* yb = reinterpret_cast<float*>(p.y[i]) + (rth - p.rt_begin[i]) * kTileRows;
 #pragma unroll
-          for (int m = 0; m < 2; ++m)
+            for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-              if (bb < p.batch) atomicAdd(yb + (size_t)bb * p.ldy[i] + row, acc[m][r] * sc[2 * m + (r >> 1)]);
-            }
-        } else if (t + 1 < b) {
-          // partial of a row tile shared with other warps / CTAs, kept in registers until every
-          // warp has left the main loop (the partial slots alias x' and the code rings). Only the
-          // head row tile can end before the range does (middle row tiles are owned); the tail
-          // partial simply stays in acc.
+              for (int r = 0; r < 4; ++r) {
+                const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
+                if (bb < p.batch)
+                  atomicAdd(yb + (size_t)bb * p.ldy[i] + row, acc[2 * h + m][r] * sc[4 * h + 2 * m + (r >> 1)]);
+              }
+          } else if (t + 1 < b) {
+            // partial of a row tile shared with other warps / CTAs, kept in registers until every
+            // warp has left the main loop (the partial slots alias x' and the code rings). Only the
+            // head row tile can end before the range does (middle row tiles are owned); the tail
+            // partial simply stays in acc.
 #pragma unroll
-          for (int m = 0; m < 2; ++m)
+            for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) hp[m][r] = acc[m][r];
+              for (int r = 0; r < 4; ++r) hp[m][r] = acc[m][r];
+          }
         }
-        if (own || p.y_atomic || t + 1 < b) {
+        if (own || RP == 2 || p.y_atomic || t + 1 < b) {
 #pragma unroll
-          for (int m = 0; m < 2; ++m)
+          for (int m = 0; m < 2 * RP; ++m)
 #pragma unroll
             for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
         }
@@ -862,10 +873,10 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
   flush_stamps(8);
 }
 
-template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, int XM>
+template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ, int XM, int RP = 1>
 cudaError_t launch_one(const GemvParams& prm, int grid, bool pdl, cudaStream_t s) {
   using PL = Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>;
-  const int smem = PL::XS_OFF + (std::max)(prm.xs_bytes + PL::NWARP * prm.ns * PL::STAGE, PL::PART);
+  const int smem = PL::XS_OFF + (std::max)(prm.xs_bytes + PL::NWARP * prm.ns * RP * PL::STAGE, PL::PART);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(PL::NWARP * 32);
@@ -876,15 +887,18 @@ cudaError_t launch_one(const GemvParams& prm, int grid, bool pdl, cudaStream_t s
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, DEQ, XM>;
+  auto k = qp_gemv_kernel<MODE, CLO, CHI, L, TB, REPS, DEQ, XM, RP>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM_MAX);
   if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k, prm);
   return e;
 }
 
 // Runtime part of the shared-memory plan: stage x' in shared memory when it fits beside at least
-// one ring stage per warp (opt-in: QP_XS=1), then as many ring stages (<= 4) as fit.
+// one ring stage per warp (opt-in: QP_XS=1), then as many ring stages (<= 4) as fit. Batch 8
+// with the atomic fp32 epilogue and a small decode table uses row-pair units (RP = 2) when d_out
+// has an even number of row tiles (QP_RP2_MIN_BATCH overrides the batch threshold; 9 disables).
 int env_no_xs();
+int rp2_min_batch();
 int fused_rht_max_rounds();   // fused rotation: most rounds of in-CTA transforms worth doing
 template <int MODE, int CLO, int CHI, int L, int TB, int REPS, bool DEQ>
 cudaError_t launch_plan(const GemvParams& prm0, int grid, bool pdl, cudaStream_t s) {
@@ -895,12 +909,14 @@ cudaError_t launch_plan(const GemvParams& prm0, int grid, bool pdl, cudaStream_t
   const int xs_bytes = rot_scratch_offset(prm.batch, rs);
   if (!DEQ && prm.x_raw) {
     // fused rotation: x' and the rotation scratch beside >= 1 ring stage per warp, and at most
-    // kMaxRotRounds rounds of NWARP / (b/256) blocks (else the caller launches the rotation kernel)
+    // fused_rht_max_rounds() rounds of NWARP / (b/256) blocks (else the caller launches the
+    // rotation kernel)
     const int spb = prm.rht_block / 256;
     const int scratch = prm.rht_block > 256 ? PX::NWARP * 256 * 4 : 0;
     const int rounds = spb >= 1 && spb <= PX::NWARP ? (prm.batch * (prm.d_in / prm.rht_block) + PX::NWARP / spb - 1) /
                                                           (PX::NWARP / spb) : 1 << 20;
-    if (rounds > fused_rht_max_rounds() || xs_bytes + scratch + PX::NWARP * PX::STAGE > PX::AVAIL) return cudaErrorNotSupported;
+    if (rounds > fused_rht_max_rounds() || xs_bytes + scratch + PX::NWARP * PX::STAGE > PX::AVAIL)
+      return cudaErrorNotSupported;
     prm.xs_bytes = xs_bytes + scratch;
     prm.xs_rs = rs;
     prm.ns = (std::min)(4, (PX::AVAIL - prm.xs_bytes) / (PX::NWARP * PX::STAGE));
@@ -914,6 +930,18 @@ cudaError_t launch_plan(const GemvParams& prm0, int grid, bool pdl, cudaStream_t
   }
   prm.xs_bytes = 0;
   prm.xs_rs = 0;
+  // row pairs only where they measured faster: batch >= rp2_min_batch() (8) with a small decode
+  // table (VQ / NUQ / UNIF), whose ring keeps >= 2 stages of two tiles
+  if (!DEQ && prm.y_atomic && prm.batch >= rp2_min_batch() && prm.RT % 2 == 0 && PL::TAB <= 32768 &&
+      PL::AVAIL >= PL::NWARP * 2 * 2 * PL::STAGE) {
+    prm.ns = (std::min)(4, PL::AVAIL / (PL::NWARP * 2 * PL::STAGE));
+    const int units = (prm.RT / 2) * prm.KT;
+    if (grid > units) {
+      grid = units;
+      prm.grid_magic = 0;                          // host reciprocal was for the larger grid
+    }
+    return launch_one<MODE, CLO, CHI, L, TB, REPS, false, 0, 2>(prm, grid, pdl, s);
+  }
   prm.ns = (std::min)(4, PL::AVAIL / (PL::NWARP * PL::STAGE));
   return launch_one<MODE, CLO, CHI, L, TB, REPS, DEQ, 0>(prm, grid, pdl, s);
 }

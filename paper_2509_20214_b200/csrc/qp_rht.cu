@@ -203,6 +203,16 @@ int fused_rht_max_rounds() {
   return n;
 }
 
+int rp2_min_batch() {
+  // smallest batch for the row-pair GEMV units (QP_RP2_MIN_BATCH; profiles/r1/ab_xs_r1.md section 9)
+  static int n = -1;
+  if (n < 0) {
+    const char* e = getenv("QP_RP2_MIN_BATCH");
+    n = e ? atoi(e) : 8;
+  }
+  return n;
+}
+
 int env_no_xs() {
   // x' staged in shared memory is opt-in (QP_XS=1): measured slower than the register path on
   // the C2 shapes (profiles/r1/ab_xs_r1.md)

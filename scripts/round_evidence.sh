@@ -16,6 +16,8 @@ QP_BENCH_EAGER=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-contro
   --log-file gpurun_out/ev_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev_ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:qp_gemv_kernel -s 4 -c 1 \
   -o gpurun_out/ev_prof_gemv python tools/prof_gemv.py --shape 14336x4096 --scheme tcq --bits-x4 10 --iters 8 > gpurun_out/ev_ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:qp_gemv_kernel -s 4 -c 1 \
+  -o gpurun_out/ev_prof_gemv_b8 python tools/prof_gemv.py --shape 14336x4096 --scheme tcq --bits-x4 10 --iters 8 --batch 8 > gpurun_out/ev_ncu_full_b8.log 2>&1
 timeout 1500 python tools/sweep.py --batches 1,2,4,8 --out gpurun_out/ev_sweep.jsonl > gpurun_out/ev_sweep.txt 2>&1
 timeout 600 python tools/decoder_layer.py --out gpurun_out/ev_c5.jsonl > gpurun_out/ev_c5.txt 2>&1
 timeout 900 python tools/sweep.py --shapes 28672x8192,8192x28672 --widths c4 --batches 1,8 --shards 1,2,4,8 \

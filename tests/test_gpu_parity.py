@@ -400,3 +400,29 @@ def test_fused_rotation_repeated_launches_in_graph():
             g.replay()
         st.synchronize()
     assert np.max(linear.normwise_error(y.cpu().numpy(), y_ref)) <= TOL
+
+
+@pytest.mark.parametrize("scheme,bits_x4", [("nuq", 16), ("vq", 12), ("tcq", 10)])
+def test_batch8_row_pair_units_and_groups(scheme, bits_x4):
+    """Batch 8 with a small decode table runs row-pair work units (RP = 2): the two row tiles of a
+    pair share the x' fragments. Covered on a fused group whose members split row pairs unevenly
+    (3 + 1 row tiles) and with fewer units than SMs (the grid shrinks), and on a ragged k range."""
+    Lb = _need_gpu()
+    shapes = [(96, 768), (32, 768)]
+    x = activations_fp16(8, 768)
+    layers, refs = [], []
+    for i, (do, di) in enumerate(shapes):
+        lay, codes, s, ocb = _layer(scheme, bits_x4, do, di, layer_id=30 + i)
+        layers.append(lay)
+        refs.append(linear.linear_from_codes(codes, do, di, scheme, bits_x4, ocb, s, x.astype(np.float64), SEED))
+    g = Lb.Group(layers)
+    ys = [torch.empty(8, do, device="cuda") for do, _ in shapes]
+    g.forward(torch.from_numpy(x).cuda(), 8, ys)
+    torch.cuda.synchronize()
+    for y, ref in zip(ys, refs):
+        assert np.max(linear.normwise_error(y.cpu().numpy(), ref)) <= TOL
+    lay, codes, s, ocb = _layer(scheme, bits_x4, 1024, 2560, layer_id=33)
+    x = activations_fp16(8, 2560)
+    y = _fwd(lay, x, 8)
+    ref = linear.linear_from_codes(codes, 1024, 2560, scheme, bits_x4, ocb, s, x.astype(np.float64), SEED)
+    assert np.max(linear.normwise_error(y, ref)) <= TOL

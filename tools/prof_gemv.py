@@ -21,7 +21,7 @@ ap.add_argument("--scheme", default="tcq")
 ap.add_argument("--bits-x4", type=int, default=10)
 ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--iters", type=int, default=5)
-ap.add_argument("--replicas", type=int, default=4)
+ap.add_argument("--replicas", type=int, default=0, help="layer copies cycled (0: enough for > 2x L2)")
 ap.add_argument("--time", action="store_true")
 ap.add_argument("--pdl", action="store_true")
 ap.add_argument("--rht", action="store_true", help="forward from raw x (rotation kernel + GEMV)")
@@ -30,6 +30,9 @@ a = ap.parse_args()
 d_out, d_in = map(int, a.shape.split("x"))
 cb = QL.Codebook(a.scheme, a.bits_x4, Q.load_fp16(a.scheme, a.bits_x4), L=16)
 r = QL.Rht(7, d_in)
+if a.replicas <= 0:
+    a.replicas = max(2, -(-2 * torch.cuda.get_device_properties(0).L2_cache_size
+                          // Q.code_bytes(d_out, d_in, a.scheme, a.bits_x4)) + 1)
 lays = [QL.Layer.from_codes(random_code_bytes(Q.code_bytes(d_out, d_in, a.scheme, a.bits_x4), i),
                             channel_scales(d_out, d_in), d_out, d_in, a.scheme, a.bits_x4, cb, r)
         for i in range(a.replicas)]
@@ -45,7 +48,7 @@ torch.cuda.synchronize()
 if a.time:
     # back-to-back launches captured in one CUDA graph (no host gaps), replicas cycle through L2
     stream = torch.cuda.Stream()
-    n = 40
+    n = max(40, 2 * a.replicas)
     flags = base | (0 if a.pdl else QL.QP_NO_PDL)
     with torch.cuda.stream(stream):
         for i in range(n):
