@@ -117,10 +117,18 @@ qp_status qp_layer_from_codes(const void* codes_host, size_t n_bytes, const floa
 /* Data-free quantization of an nn.Linear weight W[d_out][d_in] (host fp32, row-major)
  * (P:348): W' = W R^T, s_j = RMS(W'_j), W~ = W'/s, then RTN (NUQ, UNIF, VQ) or the
  * rotate-half tail-biting Viterbi (TCQ, half-TCQ; reading R4), on n_threads
- * host threads (0 = all). Host-side and slow at L = 16; the GPU encoder
- * is future work. */
+ * host threads (0 = all). Host-side and slow at L = 16 (~0.1 s per 256-weight trellis per
+ * thread): use qp_quantize_offline_gpu for TCQ layers of real size. */
 qp_status qp_quantize_offline(const float* W_host, int d_out, int d_in, qp_scheme scheme, int bits_x4,
                               const qp_codebook* cb, const qp_rht* r, int n_threads, qp_layer** out);
+
+/* qp_quantize_offline with the TCQ / half-TCQ trellis search on the current GPU:
+ * every (tile, lane) trellis is one CTA's rotate-half Viterbi in float64 with the host
+ * encoder's operation order, so the codes are bitwise those of qp_quantize_offline (rotation,
+ * scales, RTN schemes and bit packing stay on the host). Synchronous; allocates device scratch
+ * (~0.5 MB per SM at L = 16). Errors as qp_quantize_offline, plus QP_ERR_CUDA. */
+qp_status qp_quantize_offline_gpu(const float* W_host, int d_out, int d_in, qp_scheme scheme, int bits_x4,
+                                  const qp_codebook* cb, const qp_rht* r, int n_threads, qp_layer** out);
 
 /* Copy a layer's codes / scales back to the host (n_bytes must equal the stored size). */
 qp_status qp_layer_get_codes(const qp_layer* l, void* codes_host, size_t n_bytes);

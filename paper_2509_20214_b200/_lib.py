@@ -31,7 +31,7 @@ QP_FUSE_RHT = 16
 # every symbol include/qpalette.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "qp_set_allocator", "qp_codebook_load", "qp_codebook_free", "qp_rht_create", "qp_rht_free", "qp_rht_apply",
-    "qp_layer_from_codes", "qp_quantize_offline", "qp_layer_get_codes", "qp_layer_get_scales", "qp_linear_fwd",
+    "qp_layer_from_codes", "qp_quantize_offline", "qp_quantize_offline_gpu", "qp_layer_get_codes", "qp_layer_get_scales", "qp_linear_fwd",
     "qp_fuse", "qp_group_free", "qp_fused_linear", "qp_dequantize", "qp_layer_shard", "qp_nccl_unique_id",
     "qp_nccl_comm_create", "qp_nccl_comm_destroy", "qp_linear_fwd_sharded", "qp_layer_info", "qp_launch_count",
     "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range", "qp_optimal_bits",
@@ -63,6 +63,7 @@ def lib() -> C.CDLL:
             "qp_rht_apply": [vp, vp, i, i, vp, vp],
             "qp_layer_from_codes": [vp, sz, vp, i, i, i, i, vp, vp, C.POINTER(vp)],
             "qp_quantize_offline": [vp, i, i, i, i, vp, vp, i, C.POINTER(vp)],
+            "qp_quantize_offline_gpu": [vp, i, i, i, i, vp, vp, i, C.POINTER(vp)],
             "qp_layer_get_codes": [vp, vp, sz],
             "qp_layer_get_scales": [vp, vp],
             "qp_linear_fwd": [vp, vp, i, i, vp, i, C.c_uint, vp],
@@ -183,11 +184,13 @@ class Layer:
 
     @classmethod
     def quantize_offline(cls, W: np.ndarray, scheme: str, bits_x4: int, codebook: Codebook, rht: Rht,
-                         n_threads: int = 0) -> "Layer":
+                         n_threads: int = 0, gpu: bool = False) -> "Layer":
+        """gpu=True: the TCQ trellis search runs on the GPU (qp_quantize_offline_gpu)."""
         W = np.ascontiguousarray(W, dtype=np.float32)
         h = C.c_void_p()
-        check(lib().qp_quantize_offline(W.ctypes.data, W.shape[0], W.shape[1], SCHEMES[scheme], bits_x4,
-                                        codebook.h, rht.h, n_threads, C.byref(h)))
+        fn = lib().qp_quantize_offline_gpu if gpu else lib().qp_quantize_offline
+        check(fn(W.ctypes.data, W.shape[0], W.shape[1], SCHEMES[scheme], bits_x4, codebook.h, rht.h, n_threads,
+                 C.byref(h)))
         return cls(h, codebook, rht)
 
     def codes(self) -> np.ndarray:

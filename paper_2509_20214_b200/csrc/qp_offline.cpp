@@ -136,14 +136,73 @@ void put_bits(std::vector<uint32_t>& words, int pos, uint32_t value, int nbits) 
 extern "C" qp_status qp_quantize_offline(const float* W_host, int d_out, int d_in, qp_scheme scheme, int bits_x4,
                                          const qp_codebook* cb, const qp_rht* r, int n_threads, qp_layer** out);
 
+namespace qp {
+size_t tcq_viterbi_scratch_bytes(int L, int s, int grid);
+cudaError_t launch_tcq_viterbi(const double* v, int units, int L, int s, int tb, const double* tlut_dev,
+                               uint32_t* windows, uint16_t* bp_scratch, int grid, cudaStream_t st);
+}
+
+namespace {
+// Rotate-half Viterbi of every TCQ unit with k-tile class c on the GPU (qp_encode.cu): fills
+// win_all[u * 128 ..] for the units in `ids`. Bitwise the host encoder's windows.
+qp_status gpu_tcq_windows(const std::vector<double>& v_all, const std::vector<long long>& ids, int L, int s, int tb,
+                          const uint16_t* host_tlut, std::vector<uint32_t>& win_all) {
+  if (ids.empty()) return QP_OK;
+  const size_t nu = ids.size();
+  std::vector<double> v(nu * 256);
+  for (size_t i = 0; i < nu; ++i) std::memcpy(&v[i * 256], &v_all[(size_t)ids[i] * 256], 256 * sizeof(double));
+  std::vector<double> tl((size_t)2 << tb);
+  for (size_t i = 0; i < tl.size(); ++i) tl[i] = h2f(host_tlut[i]);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<size_t>((size_t)sms, nu);
+  double *d_v = nullptr, *d_tl = nullptr;
+  uint32_t* d_w = nullptr;
+  uint16_t* d_bp = nullptr;
+  cudaError_t e = cudaMalloc(&d_v, v.size() * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_tl, tl.size() * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_w, nu * 128 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&d_bp, qp::tcq_viterbi_scratch_bytes(L, s, grid));
+  if (e == cudaSuccess) e = cudaMemcpy(d_v, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_tl, tl.data(), tl.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = qp::launch_tcq_viterbi(d_v, (int)nu, L, s, tb, d_tl, d_w, d_bp, grid, nullptr);
+  std::vector<uint32_t> w(nu * 128);
+  if (e == cudaSuccess) e = cudaMemcpy(w.data(), d_w, w.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  cudaFree(d_v);
+  cudaFree(d_tl);
+  cudaFree(d_w);
+  cudaFree(d_bp);
+  if (e != cudaSuccess) return (qp_status)qp::set_error(QP_ERR_CUDA, cudaGetErrorString(e));
+  for (size_t i = 0; i < nu; ++i) std::memcpy(&win_all[(size_t)ids[i] * 128], &w[i * 128], 128 * sizeof(uint32_t));
+  return QP_OK;
+}
+}  // namespace
+
+static qp_status quantize_offline_impl(const float* W_host, int d_out, int d_in, qp_scheme scheme, int bits_x4,
+                                       const qp_codebook* cb, const qp_rht* r, int n_threads, bool gpu,
+                                       qp_layer** out);
+
+qp_status qp_quantize_offline(const float* W_host, int d_out, int d_in, qp_scheme scheme, int bits_x4,
+                              const qp_codebook* cb, const qp_rht* r, int n_threads, qp_layer** out) {
+  return quantize_offline_impl(W_host, d_out, d_in, scheme, bits_x4, cb, r, n_threads, false, out);
+}
+
+extern "C" qp_status qp_quantize_offline_gpu(const float* W_host, int d_out, int d_in, qp_scheme scheme,
+                                             int bits_x4, const qp_codebook* cb, const qp_rht* r, int n_threads,
+                                             qp_layer** out) {
+  return quantize_offline_impl(W_host, d_out, d_in, scheme, bits_x4, cb, r, n_threads, true, out);
+}
+
 // accessors implemented in qp_host.cpp (objects are opaque here)
 extern "C" {
 qp_status qp_internal_codebook_info(const qp_codebook* cb, int* L, int* tb, const uint16_t** host, size_t* n);
 qp_status qp_internal_rht_info(const qp_rht* r, uint64_t* seed, int* d_in, int* block, const uint32_t** sign_bits);
 }
 
-qp_status qp_quantize_offline(const float* W_host, int d_out, int d_in, qp_scheme scheme, int bits_x4,
-                              const qp_codebook* cb, const qp_rht* r, int n_threads, qp_layer** out) {
+static qp_status quantize_offline_impl(const float* W_host, int d_out, int d_in, qp_scheme scheme, int bits_x4,
+                                       const qp_codebook* cb, const qp_rht* r, int n_threads, bool gpu,
+                                       qp_layer** out) {
   if (!W_host || !cb || !r || !out) return QP_ERR_INVALID_ARG;
   *out = nullptr;
   int L = 0, tb = 0, rd_in = 0, block = 0;
@@ -222,6 +281,34 @@ qp_status qp_quantize_offline(const float* W_host, int d_out, int d_in, qp_schem
   const size_t rowtile_bytes = (size_t)KH * 512 * c_lo + (size_t)(KT - KH) * 512 * c_hi;
   std::vector<uint8_t> codes(rowtile_bytes * RT, 0);
   const long long units = (long long)RT * KT * 32;
+  // the trellis input of unit u (tile u / 32, lane u % 32): 128 weight pairs in step order
+  auto gather = [&](long long u, double* v) {
+    const int lane = (int)(u % 32);
+    const long long tile = u / 32;
+    const int rt = (int)(tile / KT), kt = (int)(tile % KT);
+    for (int j = 0; j < 128; ++j) {
+      int row, col;
+      step_pos(lane, j, &row, &col);
+      const double* src = Wt.data() + (size_t)(rt * 32 + row) * d_in + kt * 256 + col;
+      v[2 * j] = src[0];
+      v[2 * j + 1] = src[1];
+    }
+  };
+  std::vector<uint32_t> gpu_win;   // GPU-encoded windows of every TCQ unit [units][128]
+  if (tcq && gpu) {
+    std::vector<double> v_all((size_t)units * 256);
+    for (long long u = 0; u < units; ++u) gather(u, &v_all[(size_t)u * 256]);
+    gpu_win.resize((size_t)units * 128);
+    std::vector<long long> lo, hi;
+    for (long long u = 0; u < units; ++u) (((u / 32) % KT) < KH ? lo : hi).push_back(u);
+    if (c_lo == c_hi) {
+      lo.insert(lo.end(), hi.begin(), hi.end());
+      hi.clear();
+      std::sort(lo.begin(), lo.end());
+    }
+    if ((st = gpu_tcq_windows(v_all, lo, L, c_lo, tb, host, gpu_win)) != QP_OK) return st;
+    if ((st = gpu_tcq_windows(v_all, hi, L, c_hi, tb, host, gpu_win)) != QP_OK) return st;
+  }
   std::atomic<long long> next{0};
   auto worker = [&]() {
     std::vector<double> v(256);
@@ -244,7 +331,10 @@ qp_status qp_quantize_offline(const float* W_host, int d_out, int d_in, qp_schem
       }
       std::vector<uint32_t> words(4 * c, 0u);
       if (tcq) {
-        tcq_encode(kt < KH ? vlo : vhi, v.data(), win.data());
+        if (gpu)
+          std::memcpy(win.data(), &gpu_win[(size_t)u * 128], 128 * sizeof(uint32_t));
+        else
+          tcq_encode(kt < KH ? vlo : vhi, v.data(), win.data());
         for (int j = 0; j < 128; ++j) put_bits(words, j * c, win[j] >> (L - c), c);   // top s bits of w_j
       } else if (scheme == QP_VQ) {
         const int ne = 1 << c;

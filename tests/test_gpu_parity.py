@@ -426,3 +426,30 @@ def test_batch8_row_pair_units_and_groups(scheme, bits_x4):
     y = _fwd(lay, x, 8)
     ref = linear.linear_from_codes(codes, 1024, 2560, scheme, bits_x4, ocb, s, x.astype(np.float64), SEED)
     assert np.max(linear.normwise_error(y, ref)) <= TOL
+
+
+@pytest.mark.parametrize("d_out,d_in,scheme,bits_x4,L", [
+    (256, 256, "tcq", 8, 12),        # config C1
+    (32, 512, "tcq", 10, 16),        # TCQ-2.5, L = 16: 1 x 2 tiles = 64 trellises
+    (32, 512, "half_tcq", 13, 16),   # half-TCQ 3.25: k tile 0 at s = 6, k tile 1 at s = 7
+])
+def test_gpu_trellis_encoder_matches_host_and_oracle(d_out, d_in, scheme, bits_x4, L):
+    """qp_quantize_offline_gpu (NEXT-1): the rotate-half Viterbi on the GPU, float64 in the host
+    encoder's operation order, yields bitwise the host encoder's codes; its total distortion equals
+    the oracle's rotate-half encoder's (path cost, reading R5)."""
+    Lb = _need_gpu()
+    from qp_synth import gaussian_weights
+    cb, ocb = _pair(scheme, bits_x4, L=L)
+    W = gaussian_weights(d_out, d_in, seed=0).astype(np.float32)
+    r = Lb.Rht(SEED, d_in)
+    lay_g = Lb.Layer.quantize_offline(W, scheme, bits_x4, cb, r, gpu=True)
+    lay_h = Lb.Layer.quantize_offline(W, scheme, bits_x4, cb, r)
+    codes_g, codes_h = lay_g.codes(), lay_h.codes()
+    assert np.array_equal(codes_g, codes_h)
+    assert np.array_equal(lay_g.scales(), lay_h.scales())
+    Wt, _ = linear.gaussianize(W.astype(np.float64), SEED)
+    codes_o, _ = linear.quantize_offline(W.astype(np.float64), scheme, bits_x4, ocb, SEED)
+    Wg = decode.decode_layer(codes_g, d_out, d_in, scheme, bits_x4, ocb)
+    Wo = decode.decode_layer(codes_o, d_out, d_in, scheme, bits_x4, ocb)
+    dg, do = np.sum((Wg - Wt) ** 2), np.sum((Wo - Wt) ** 2)
+    assert abs(dg - do) / do < 1e-6
