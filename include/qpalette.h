@@ -177,6 +177,18 @@ qp_status qp_shard_range(int d_out, int d_in, qp_scheme scheme, int bits_x4, int
  * QP_ERR_CONFIG_MISMATCH (infeasible: M < eta * sum n). */
 qp_status qp_optimal_bits(const double* a, const double* n, int L, double M, double eta, double* b_out);
 
+/* Host-only: fusion-aware mixed-scheme quantization, solved exactly. For n_blocks
+ * Transformer blocks with layers (q, k, v, o, u, g, d), sensitivities a[b*7 + l], quantizer
+ * distortions err[q] (data-free loss a_l * err_q) and profiled latencies cost[t*n_quant
+ * + q] of group type t in (q, k, v, qk, qv, kv, qkv, o, u, g, ug, d) quantized by q, choose the
+ * fusible groups and one quantizer per group minimising the total loss with total cost <= budget
+ * (fusion = 0: singleton groups only, the plain MSQ of P:436-440). Outputs per layer b*7 + l: the
+ * group type it belongs to (group_out) and its quantizer (quant_out); optional totals. Exact
+ * multiple-choice-knapsack solution by Pareto frontiers. Errors: QP_ERR_INVALID_ARG,
+ * QP_ERR_CONFIG_MISMATCH (budget below the cheapest assignment), QP_ERR_ALLOC (frontier > 4 M). */
+qp_status qp_plan_msq(int n_blocks, const double* a, int n_quant, const double* err, const double* cost,
+                      double budget, int fusion, int* group_out, int* quant_out, double* loss_out, double* cost_out);
+
 /* NCCL plumbing for the row-sharded path (NCCL over NVLink / NVSwitch).
  * qp_nccl_unique_id writes 128 bytes; broadcast them (e.g. with torch.distributed)
  * and call qp_nccl_comm_create on every rank. comm is an ncclComm_t. */

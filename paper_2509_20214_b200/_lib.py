@@ -34,7 +34,7 @@ EXPORTS = [
     "qp_layer_from_codes", "qp_quantize_offline", "qp_quantize_offline_gpu", "qp_layer_get_codes", "qp_layer_get_scales", "qp_linear_fwd",
     "qp_fuse", "qp_group_free", "qp_fused_linear", "qp_dequantize", "qp_layer_shard", "qp_nccl_unique_id",
     "qp_nccl_comm_create", "qp_nccl_comm_destroy", "qp_linear_fwd_sharded", "qp_layer_info", "qp_launch_count",
-    "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range", "qp_optimal_bits",
+    "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range", "qp_optimal_bits", "qp_plan_msq",
 ]
 
 
@@ -75,6 +75,8 @@ def lib() -> C.CDLL:
             "qp_shard_range": [i, i, i, i, i, i, C.POINTER(i), C.POINTER(i), C.POINTER(sz), C.POINTER(sz)],
             "qp_optimal_bits": [C.POINTER(C.c_double), C.POINTER(C.c_double), i, C.c_double, C.c_double,
                                 C.POINTER(C.c_double)],
+            "qp_plan_msq": [i, C.POINTER(C.c_double), i, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double, i,
+                            C.POINTER(i), C.POINTER(i), C.POINTER(C.c_double), C.POINTER(C.c_double)],
             "qp_nccl_unique_id": [vp],
             "qp_nccl_comm_create": [vp, i, i, C.POINTER(vp)],
             "qp_nccl_comm_destroy": [vp],
@@ -278,3 +280,18 @@ def optimal_bits(a, n, M: float, eta: float) -> np.ndarray:
     check(lib().qp_optimal_bits(a.ctypes.data_as(dp), n.ctypes.data_as(dp), len(a), float(M), float(eta),
                                 out.ctypes.data_as(dp)))
     return out
+
+
+def plan_msq(a, err, cost, budget: float, fusion: bool = True):
+    """qp_plan_msq (host-only): a [B][7], err [nq], cost [12][nq] -> (loss, cost, group [B][7], quant [B][7])."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    err = np.ascontiguousarray(err, dtype=np.float64)
+    cost = np.ascontiguousarray(cost, dtype=np.float64)
+    B, nq = a.shape[0], err.shape[0]
+    g = np.full((B, 7), -1, dtype=np.int32)
+    q = np.full((B, 7), -1, dtype=np.int32)
+    lo, co = C.c_double(), C.c_double()
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int)
+    check(lib().qp_plan_msq(B, a.ctypes.data_as(dp), nq, err.ctypes.data_as(dp), cost.ctypes.data_as(dp), float(budget),
+                            1 if fusion else 0, g.ctypes.data_as(ip), q.ctypes.data_as(ip), C.byref(lo), C.byref(co)))
+    return lo.value, co.value, g, q

@@ -453,3 +453,26 @@ def test_gpu_trellis_encoder_matches_host_and_oracle(d_out, d_in, scheme, bits_x
     Wo = decode.decode_layer(codes_o, d_out, d_in, scheme, bits_x4, ocb)
     dg, do = np.sum((Wg - Wt) ** 2), np.sum((Wo - Wt) ** 2)
     assert abs(dg - do) / do < 1e-6
+
+
+@pytest.mark.parametrize("scheme,bits_x4,paper,tol", [
+    ("tcq", 8, 0.07101, 0.02),    # P:909 Ours-TCQ-2 (L = 16, T = 256, tlut_bits = 9)
+    ("vq", 8, 0.10857, 0.02),     # P:911 Ours-VQ-2 (our k-means codebook: reading R21)
+    ("nuq", 8, 0.11747, 0.005),   # P:910 Ours-NUQ-2
+])
+def test_table5_distortion_at_scale(scheme, bits_x4, paper, tol):
+    """Table 5 at real scale through the product: a 1024x4096 N(0,1) matrix quantized by
+    qp_quantize_offline_gpu (TCQ trellis search on the GPU, L = 16), decoded by qp_dequantize;
+    the mean squared error against the oracle's standardized weights W~ matches the paper's
+    distortion (4 M samples: sampling std ~2e-5)."""
+    Lb = _need_gpu()
+    from qp_synth import gaussian_weights
+    cb, _ = _pair(scheme, bits_x4, L=16)
+    d_out, d_in = 1024, 4096
+    W = gaussian_weights(d_out, d_in, seed=0).astype(np.float32)
+    lay = Lb.Layer.quantize_offline(W, scheme, bits_x4, cb, Lb.Rht(SEED, d_in), gpu=True)
+    W_hat = _dequant_gpu(lay).astype(np.float64)
+    Wt, _ = linear.gaussianize(W.astype(np.float64), SEED)
+    d = float(np.mean((Wt - W_hat) ** 2))
+    assert abs(d - paper) / paper < tol, d
+    assert d >= 2.0 ** (-2 * bits_x4 / 4)       # rate-distortion bound (P:162)
