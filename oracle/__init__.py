@@ -14,6 +14,8 @@ Modules
   decode     dq(r; LUT) for TCQ, half-TCQ, VQ, NUQ, UNIF
   encode     RTN and tail-biting Viterbi
   linear     y = diag(s) W_hat R x and the data-free offline path
+  allocation Theorem 1 optimal fractional bit allocation
+  msq        fusion-aware mixed-scheme quantization by brute force (tiny instances)
 
 Parity status of every function is listed in DESIGN.md ("Oracle pins");
 functions without an external pin say "parity unpinned" in their docstring.
