@@ -561,6 +561,15 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
   // dependent launch it overlaps the previous kernel: the code copies are in flight (issued
   // above) while the table words arrive from L2 and are expanded into the replicated image.
   stamp(7);
+#ifdef QP_X_EARLY
+  // (experiment) wait for the producer and request the first tile's activations before the table
+  // expansion, so their L2 latency hides under the 128 KB of shared stores
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (XM == 0 && xrow && a < b) {
+    load_x8(xb, xlane + kt * kTileCols);
+    load_x8(xb + 8, xlane + kt * kTileCols + 16);
+  }
+#endif
   tb.store(tab);
   stamp(6);
   for (int st = 1; st < NS; ++st) {                // the rest of the ring's first fill
@@ -573,7 +582,9 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
   // the GEMV CTAs; profiles/r1/ab_xs_r1.md section 8)
   asm volatile("griddepcontrol.launch_dependents;");
 #endif
+#ifndef QP_X_EARLY
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   stamp(5);
   // this lane's x' row in the staged copy (lanes without a batch row read row batch-1: their
   // products land in y columns that are never stored)
@@ -615,8 +626,10 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
     }
     rotate_x<NWARP>(p, smem + PL::XS_OFF, reinterpret_cast<float*>(smem + PL::XS_OFF + rot_scratch_offset(p.batch, p.xs_rs)));
   } else if (xrow && a < b) {                      // first tile, kappa 0..7
+#ifndef QP_X_EARLY
     load_x8(xb, xlane + kt * kTileCols);
     load_x8(xb + 8, xlane + kt * kTileCols + 16);
+#endif
   }
   __syncthreads();
   auto scale_of = [&](uint32_t rt_, int row) -> float { return __ldg(p.scales + rt_ * kTileRows + row); };
@@ -662,6 +675,16 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
         const uint32_t last = (CLO == CHI || c == CMAX) ? cur[4 * CMAX - 1] : cur[4 * CLO - 1];
         const uint32_t dep = __reduce_or_sync(0xffffffffu, last & p.zero);
         if (lane == 0 && t + NS < b) fetch(f_ptr, tile_bytes(kt_f), st, dep);
+#ifdef QP_L2_PREFETCH
+        // warm L2 with the unit after the one just requested (its bulk copy then hits L2)
+        if (lane == 0 && t + NS + 1 < b) {
+          const uint8_t* nx = f_ptr + tile_bytes(kt_f) + (kt_f + 1 == (int)KT ? (RP - 1) * rowtile_bytes : 0);
+#pragma unroll
+          for (int hh = 0; hh < RP; ++hh)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(nx + hh * rowtile_bytes),
+                         "r"(tile_bytes(kt_f + 1 == (int)KT ? 0 : kt_f + 1)) : "memory");
+        }
+#endif
         advance_f();
       }
       const __half* x_hi = (!XS && xrow && h == 0) ? xlane + kt * kTileCols + 32 : nullptr;
