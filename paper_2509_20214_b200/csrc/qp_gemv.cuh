@@ -2,26 +2,30 @@
 //
 // y[beta][row] = s[row] * sum_k W_hat[row][k] * x'[beta][k],  batch <= 8
 //
-// Design (DESIGN.md "Kernel: fused dequant-GEMV"):
-//  * persistent grid, one CTA per SM (128 KB replicated decode table in shared memory);
-//    the RT x KT tiles (32 rows x 256 cols, LAYOUT.md) are split into contiguous,
-//    k-minor ranges per CTA and per warp (flat stream-K: balanced to within one tile);
+// Design (DESIGN.md section 6.1):
+//  * persistent grid, one CTA per SM, 16 warps (12 above 4 bits/weight); a replicated decode
+//    table in shared memory (entries x 32 replicas, bank = lane: 128 KB for TCQ tb = 9);
+//    the RT x KT tiles (32 rows x 256 cols, LAYOUT.md) are split into contiguous, k-minor
+//    ranges per CTA and per warp (flat stream-K: balanced to within one tile). Work units are
+//    single tiles, or row pairs (RP = 2: the two row tiles share the activation fragments) at
+//    batch 8 with small tables;
 //  * each lane owns one 256-weight trellis / code run per tile. A tile's codes are one
-//    contiguous 512c-byte block; every warp streams its tiles into a private NS-stage ring in
+//    contiguous 512c-byte block; every warp streams its units into a private NS-stage ring in
 //    shared memory with 1-D bulk-async copies (cp.async.bulk, the TMA engine; one elected lane
-//    issues them, completion on a per-stage mbarrier), NS tiles ahead of the decode, so code
-//    loads never block instruction issue (the register-prefetch design stalled the prologue's
-//    table build behind ~40 KB/SM of outstanding LDGs). Each lane then reads its 4c stream
-//    words with c conflict-free 128-bit shared loads;
-//  * decode per weight pair (TCQ): funnel-shift window -> hash (w+1)w -> masked key ->
-//    one conflict-free LDS from a 32-way replicated table (bank = lane) -> half2;
-//    VQ/NUQ/UNIF: funnel-shift index -> LDS. Pairs land directly in mma.sync m16n8k16
-//    A-fragment registers (the layout was chosen so that step j IS fragment register j);
-//    the activations are the B fragment (batch in N <= 8), fp32 accumulation;
-//  * epilogue: per-row scale, then warp partials -> CTA smem reduction -> deterministic
-//    cross-CTA fixup (last-arriving CTA sums the partials in CTA order) -> y.
-//  * Programmatic dependent launch: table build and the first code loads happen before
-//    griddepcontrol.wait (they read only immutable layer data).
+//    issues them, completion on a per-stage mbarrier) and refills a stage as soon as it is read
+//    (ordered by a warp reduction over the loaded words), so code loads never block instruction
+//    issue. Each lane reads its 4c stream words with c conflict-free 128-bit shared loads;
+//  * decode per weight pair (TCQ): funnel-shift window -> IMAD hash (w+1)w -> IMAD key shift ->
+//    LOP3 mask|lane -> one conflict-free LDS (bank = lane) -> half2; VQ/NUQ/UNIF: shift ->
+//    LOP3 -> LDS. Pairs land directly in mma.sync m16n8k16 A-fragment registers (step j IS
+//    fragment register j); the activations are the B fragment (batch in N <= 8; one 256-bit
+//    load per lane per half tile, or shared memory with XM >= 1), fp32 accumulation;
+//  * epilogue: per-row scales prefetched per row tile; owned row tiles stored directly; split
+//    row tiles red.add into a pre-zeroed fp32 y, or (fp16 y / QP_DETERMINISTIC) warp partials ->
+//    CTA shared-memory reduction -> in-order cross-CTA fixup;
+//  * programmatic dependent launch: table build and the first code copies happen before
+//    griddepcontrol.wait (they read only immutable layer data); dependents are triggered after
+//    the main loop.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>

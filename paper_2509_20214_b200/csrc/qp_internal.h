@@ -19,7 +19,6 @@ enum DecMode : int {
 constexpr int kMaxGroup = 8;        // members of a fused group
 constexpr int kTileRows = 32;
 constexpr int kTileCols = 256;
-constexpr int kSmemTableBytes = 131072;
 constexpr int kMaxSideCtas = 16;   // preceding-kernel CTAs the GEMV grid steps aside for (run_gemv)
 
 // Static description of one kernel variant.
