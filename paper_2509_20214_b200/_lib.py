@@ -73,6 +73,7 @@ def lib() -> C.CDLL:
             "qp_dequantize": [vp, vp, vp],
             "qp_layer_shard": [vp, i, i, C.POINTER(vp)],
             "qp_shard_range": [i, i, i, i, i, i, C.POINTER(i), C.POINTER(i), C.POINTER(sz), C.POINTER(sz)],
+            "qp_set_allocator": [vp, vp, vp],
             "qp_optimal_bits": [C.POINTER(C.c_double), C.POINTER(C.c_double), i, C.c_double, C.c_double,
                                 C.POINTER(C.c_double)],
             "qp_plan_msq": [i, C.POINTER(C.c_double), i, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double, i,
@@ -295,3 +296,33 @@ def plan_msq(a, err, cost, budget: float, fusion: bool = True):
     check(lib().qp_plan_msq(B, a.ctypes.data_as(dp), nq, err.ctypes.data_as(dp), cost.ctypes.data_as(dp), float(budget),
                             1 if fusion else 0, g.ctypes.data_as(ip), q.ctypes.data_as(ip), C.byref(lo), C.byref(co)))
     return lo.value, co.value, g, q
+
+
+_ALLOC_CB = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+_FREE_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+_allocator_refs = None
+
+
+def use_torch_allocator(enable: bool = True) -> None:
+    """Route the library's device allocations (codes, scales, tables, workspaces) through
+    PyTorch's caching allocator (qp_set_allocator), so one memory pool serves both. Affects
+    objects created afterwards; free them before disabling."""
+    global _allocator_refs
+    import torch
+    if not enable:
+        check(lib().qp_set_allocator(None, None, None))
+        _allocator_refs = None
+        return
+
+    def alloc(n, ctx):
+        try:
+            return int(torch.cuda.caching_allocator_alloc(max(int(n), 1)))
+        except Exception:           # out of memory -> NULL -> QP_ERR_ALLOC
+            return None
+
+    def free(ptr, ctx):
+        if ptr:
+            torch.cuda.caching_allocator_delete(int(ptr))
+
+    _allocator_refs = (_ALLOC_CB(alloc), _FREE_CB(free))     # keep the thunks alive
+    check(lib().qp_set_allocator(C.cast(_allocator_refs[0], C.c_void_p), C.cast(_allocator_refs[1], C.c_void_p), None))

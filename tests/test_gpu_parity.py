@@ -476,3 +476,23 @@ def test_table5_distortion_at_scale(scheme, bits_x4, paper, tol):
     d = float(np.mean((Wt - W_hat) ** 2))
     assert abs(d - paper) / paper < tol, d
     assert d >= 2.0 ** (-2 * bits_x4 / 4)       # rate-distortion bound
+
+
+def test_torch_caching_allocator_backs_layers():
+    """qp_set_allocator through the binding: a layer allocated from PyTorch's caching allocator
+    computes the same y, and its memory shows up in torch's accounting."""
+    Lb = _need_gpu()
+    _pair("tcq", 10)        # codebook and rotation are cached across tests: create them (and so
+    _rht(1024)              # later free them) with the default allocator
+    try:
+        before = torch.cuda.memory_allocated()
+        Lb.use_torch_allocator(True)
+        lay, codes, s, ocb = _layer("tcq", 10, 256, 1024, layer_id=40)
+        assert torch.cuda.memory_allocated() - before >= lay.code_bytes
+        x = activations_fp16(2, 1024)
+        y = _fwd(lay, x, 2)
+        ref = linear.linear_from_codes(codes, 256, 1024, "tcq", 10, ocb, s, x.astype(np.float64), SEED)
+        assert np.max(linear.normwise_error(y, ref)) <= TOL
+        del lay
+    finally:
+        Lb.use_torch_allocator(False)
