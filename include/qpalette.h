@@ -201,6 +201,26 @@ qp_status qp_nccl_comm_destroy(void* comm);
 qp_status qp_linear_fwd_sharded(const qp_layer* shard, const void* x, qp_dtype xt, int batch, void* y_full,
                                 qp_dtype yt, void* comm, unsigned flags, void* stream);
 
+/* Row-sharded forward with the all-gather fused into the GEMV epilogue (peer
+ * memory over NVLink / NVSwitch instead of ncclAllGather): every final y value of this rank's rows
+ * is stored directly into all `world` ranks' y_full ([batch][world * shard_d_out], dtype yt in
+ * {F16, F32}, rank r's rows at columns [r*m, (r+1)*m)); then the grid's last CTA increments this
+ * rank's counter in every rank's flag array, and a one-thread wait kernel on `stream` returns once
+ * every rank has delivered into this rank's y_full, so later work on `stream` sees the whole
+ * vector. y_peers[k] / flag_peers[k]: rank k's y_full and flag array (unsigned[world + 1], zeroed
+ * once at setup, mapped into this process with qp_ipc_open; this rank's own pointers at k = rank).
+ * Uses the in-order (QP_DETERMINISTIC) epilogue; QP_Y_ACCUMULATE / QP_FUSE_RHT are rejected.
+ * Errors: QP_ERR_INVALID_ARG, plus qp_linear_fwd's. Graph-capturable (no host-side epoch). */
+qp_status qp_linear_fwd_sharded_p2p(const qp_layer* shard, const void* x, qp_dtype xt, int batch,
+                                    void* const* y_peers, unsigned* const* flag_peers, int rank, int world,
+                                    qp_dtype yt, unsigned flags, void* stream);
+
+/* CUDA IPC plumbing for qp_linear_fwd_sharded_p2p: export a device allocation's 64-byte handle,
+ * map a peer's handle into this process (peer access enabled lazily), unmap it. */
+qp_status qp_ipc_handle(const void* dev_ptr, void* handle64);
+qp_status qp_ipc_open(const void* handle64, void** dev_ptr);
+qp_status qp_ipc_close(void* dev_ptr);
+
 /* Introspection. bits_per_weight counts code bits only (reading R19). */
 qp_status qp_layer_info(const qp_layer* l, size_t* code_bytes, double* bits_per_weight, int* d_out, int* d_in);
 

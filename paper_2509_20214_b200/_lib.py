@@ -35,6 +35,7 @@ EXPORTS = [
     "qp_fuse", "qp_group_free", "qp_fused_linear", "qp_dequantize", "qp_layer_shard", "qp_nccl_unique_id",
     "qp_nccl_comm_create", "qp_nccl_comm_destroy", "qp_linear_fwd_sharded", "qp_layer_info", "qp_launch_count",
     "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range", "qp_optimal_bits", "qp_plan_msq",
+    "qp_linear_fwd_sharded_p2p", "qp_ipc_handle", "qp_ipc_open", "qp_ipc_close",
 ]
 
 
@@ -74,6 +75,10 @@ def lib() -> C.CDLL:
             "qp_layer_shard": [vp, i, i, C.POINTER(vp)],
             "qp_shard_range": [i, i, i, i, i, i, C.POINTER(i), C.POINTER(i), C.POINTER(sz), C.POINTER(sz)],
             "qp_set_allocator": [vp, vp, vp],
+            "qp_linear_fwd_sharded_p2p": [vp, vp, i, i, vp, vp, i, i, i, C.c_uint, vp],
+            "qp_ipc_handle": [vp, vp],
+            "qp_ipc_open": [vp, C.POINTER(vp)],
+            "qp_ipc_close": [vp],
             "qp_optimal_bits": [C.POINTER(C.c_double), C.POINTER(C.c_double), i, C.c_double, C.c_double,
                                 C.POINTER(C.c_double)],
             "qp_plan_msq": [i, C.POINTER(C.c_double), i, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double, i,
@@ -326,3 +331,52 @@ def use_torch_allocator(enable: bool = True) -> None:
 
     _allocator_refs = (_ALLOC_CB(alloc), _FREE_CB(free))     # keep the thunks alive
     check(lib().qp_set_allocator(C.cast(_allocator_refs[0], C.c_void_p), C.cast(_allocator_refs[1], C.c_void_p), None))
+
+
+class PeerGather:
+    """Fused all-gather destination for row-sharded layers (qp_linear_fwd_sharded_p2p): every
+    rank allocates y_full [batch][world * m] and a flag array, exchanges CUDA IPC handles through
+    torch.distributed (`group`, any backend) and maps its peers' buffers. world == 1 needs no
+    process group."""
+
+    def __init__(self, world: int, rank: int, m: int, batch: int, dtype=None, group=None):
+        import torch
+        dtype = dtype or torch.float32
+        self.world, self.rank, self.m, self.batch = world, rank, m, batch
+        self.y = torch.zeros(batch, world * m, dtype=dtype, device="cuda")
+        self.flags = torch.zeros(world + 1, dtype=torch.int32, device="cuda")
+        self._opened = []
+        if world == 1:
+            ys, fs = [self.y.data_ptr()], [self.flags.data_ptr()]
+        else:
+            import torch.distributed as dist
+            hy, hf = (C.c_char * 64)(), (C.c_char * 64)()
+            check(lib().qp_ipc_handle(C.c_void_p(self.y.data_ptr()), hy))
+            check(lib().qp_ipc_handle(C.c_void_p(self.flags.data_ptr()), hf))
+            allh = [None] * world
+            dist.all_gather_object(allh, (bytes(hy), bytes(hf)), group=group)
+            ys, fs = [], []
+            for k, (by, bf) in enumerate(allh):
+                if k == rank:
+                    ys.append(self.y.data_ptr())
+                    fs.append(self.flags.data_ptr())
+                    continue
+                py, pf = C.c_void_p(), C.c_void_p()
+                check(lib().qp_ipc_open(by, C.byref(py)))
+                check(lib().qp_ipc_open(bf, C.byref(pf)))
+                self._opened += [py.value, pf.value]
+                ys.append(py.value)
+                fs.append(pf.value)
+            torch.cuda.synchronize()
+            dist.barrier(group=group)
+        self._ys = (C.c_void_p * world)(*ys)
+        self._fs = (C.c_void_p * world)(*fs)
+
+    def forward(self, shard: "Layer", x, flags: int = 0, stream=None) -> None:
+        check(lib().qp_linear_fwd_sharded_p2p(shard.h, _ptr(x), _dtype_code(x), self.batch, self._ys, self._fs,
+                                              self.rank, self.world, _dtype_code(self.y), flags, _stream(stream)))
+
+    def close(self):
+        for p in self._opened:
+            lib().qp_ipc_close(C.c_void_p(p))
+        self._opened = []

@@ -348,11 +348,38 @@ __device__ __forceinline__ void store_out(const GemvParams& p, int rt, int row, 
   while (i + 1 < p.n_out && rt >= p.rt_begin[i + 1]) ++i;
   const int grow = (rt - p.rt_begin[i]) * kTileRows + row;
   v *= scale;
+  if (p.n_peers > 0) {
+    // fused all-gather: the final value goes straight into every rank's y_full over NVLink
+    // (peer stores through the mapped pointers; rank-local for this rank)
+    const size_t off = (size_t)b * p.peer_ld + p.peer_row0 + grow;
+#pragma unroll 1
+    for (int k = 0; k < p.n_peers; ++k) {
+      if (p.y_f32) reinterpret_cast<float*>(p.peer_y[k])[off] = v;
+      else reinterpret_cast<__half*>(p.peer_y[k])[off] = __float2half_rn(v);
+    }
+    return;
+  }
   if (p.y_f32) {
     float* dst = reinterpret_cast<float*>(p.y[i]) + (size_t)b * p.ldy[i] + grow;
     *dst = p.y_accum ? *dst + v : v;        // the owning warp is the only writer of this element
   }
   else reinterpret_cast<__half*>(p.y[i])[(size_t)b * p.ldy[i] + grow] = __float2half_rn(v);
+}
+
+// Fused all-gather completion: after every CTA's stores, the grid's last CTA increments this
+// rank's arrival flag on every peer (system scope); qp_peer_wait_kernel on each rank waits for
+// all ranks' flags. Fence / relaxed-atomic / fence gives the release-acquire chain.
+__device__ __forceinline__ void peer_signal(const GemvParams& p) {
+  if (p.n_peers <= 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(p.peer_counter, 1) == (int)gridDim.x - 1) {
+      p.peer_counter[0] = 0;                      // self-reset for the next launch
+      __threadfence_system();
+      for (int k = 0; k < p.n_peers; ++k) atomicAdd_system(p.peer_flag[k] + p.peer_rank, 1u);
+    }
+  }
 }
 
 
@@ -783,6 +810,9 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
   asm volatile("griddepcontrol.launch_dependents;");
 #endif
   if (DEQ || nC <= 0 || p.y_atomic) {
+    if constexpr (!DEQ) {
+      if (nC <= 0) peer_signal(p);                // (the fused all-gather runs the in-order path)
+    }
     flush_stamps(3);
     return;
   }
@@ -897,6 +927,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
   }
   __syncthreads();
   stamp(3);
+  peer_signal(p);
   flush_stamps(8);
 }
 

@@ -352,11 +352,30 @@ struct FusedRot {
   bool zero_y;
 };
 
+// Fused all-gather destination for run_gemv (qp_linear_fwd_sharded_p2p)
+struct PeerOut {
+  int world, rank, row0, ld;
+  void* const* y;
+  unsigned* const* flag;
+};
+thread_local const PeerOut* g_peer_out = nullptr;   // set around one run_gemv call
+
 qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, const int* rt_begin, void* const* ys,
                    const int* ldy, qp_dtype yt, bool pdl, cudaStream_t s, bool y_atomic, int side_ctas = 0,
                    const FusedRot* fr = nullptr, bool* unsupported = nullptr, bool y_accum = false) {
   GemvParams p{};
   p.y_accum = y_accum ? 1 : 0;
+  if (g_peer_out) {
+    p.n_peers = g_peer_out->world;
+    for (int k = 0; k < g_peer_out->world; ++k) {
+      p.peer_y[k] = g_peer_out->y[k];
+      p.peer_flag[k] = g_peer_out->flag[k];
+    }
+    p.peer_rank = g_peer_out->rank;
+    p.peer_row0 = g_peer_out->row0;
+    p.peer_ld = g_peer_out->ld;
+    p.peer_counter = l->d_counters + l->d_out / kTileRows;   // (the fused-rotation barrier's slot)
+  }
   if (fr) {
     p.x_raw = fr->x;
     p.x_dtype = (int)fr->xt;
@@ -931,6 +950,52 @@ qp_status qp_linear_fwd_sharded(const qp_layer* shard, const void* x, qp_dtype x
 }  // extern "C"
 
 // accessors for qp_offline.cpp (not part of the public ABI)
+extern "C" qp_status qp_linear_fwd_sharded_p2p(const qp_layer* shard, const void* x, qp_dtype xt, int batch,
+                                               void* const* y_peers, unsigned* const* flag_peers, int rank,
+                                               int world, qp_dtype yt, unsigned flags, void* stream) {
+  if (!shard || !y_peers || !flag_peers) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_linear_fwd_sharded_p2p");
+  if (world < 1 || world > kMaxGroup || rank < 0 || rank >= world)
+    return fail(QP_ERR_INVALID_ARG, "rank %d / world %d (1..%d ranks)", rank, world, kMaxGroup);
+  for (int k = 0; k < world; ++k)
+    if (!y_peers[k] || !flag_peers[k]) return fail(QP_ERR_INVALID_ARG, "peer %d pointer is NULL", k);
+  if (flags & (QP_Y_ACCUMULATE | QP_FUSE_RHT))
+    return fail(QP_ERR_INVALID_ARG, "qp_linear_fwd_sharded_p2p: QP_Y_ACCUMULATE / QP_FUSE_RHT not supported");
+  // every final value is written once, by its owner, to every rank: the in-order epilogue
+  const PeerOut po{world, rank, rank * shard->d_out, world * shard->d_out, y_peers, flag_peers};
+  g_peer_out = &po;
+  const qp_status st = qp_linear_fwd(shard, x, xt, batch, y_peers[rank], yt, flags | QP_DETERMINISTIC, stream);
+  g_peer_out = nullptr;
+  if (st != QP_OK) return st;
+  cudaError_t e = launch_peer_wait(flag_peers[rank], world, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "peer wait kernel launch");
+  return QP_OK;
+}
+
+extern "C" qp_status qp_ipc_handle(const void* dev_ptr, void* handle64) {
+  if (!dev_ptr || !handle64) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_ipc_handle");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle64, &h, 64);
+  return QP_OK;
+}
+
+extern "C" qp_status qp_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!dev_ptr || !handle64) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_ipc_open");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return QP_OK;
+}
+
+extern "C" qp_status qp_ipc_close(void* dev_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return QP_OK;
+}
+
 extern "C" qp_status qp_internal_codebook_info(const qp_codebook* cb, int* L, int* tb, const uint16_t** host,
                                                size_t* n) {
   if (!cb) return fail(QP_ERR_INVALID_ARG, "codebook is NULL");

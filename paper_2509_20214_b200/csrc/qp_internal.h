@@ -68,6 +68,14 @@ struct GemvParams {
   float rht_scale;             // 1/sqrt(b)
   int zero_y;                  // 1: zero the fp32 outputs in-kernel before accumulating into them
   int* bar_count;              // [2] grid arrival counter + generation (self-resetting)
+  // fused all-gather over peer memory (qp_linear_fwd_sharded_p2p): every final y value of this
+  // rank's rows is stored into all n_peers ranks' y_full (mapped here) at column peer_row0 + row;
+  // the grid's last CTA then bumps flag[rank] on every peer (system scope)
+  int n_peers;
+  void* peer_y[kMaxGroup];
+  unsigned* peer_flag[kMaxGroup];
+  int peer_rank, peer_row0, peer_ld;
+  int* peer_counter;           // grid arrival counter (self-resetting)
   // cross-CTA fixup workspace
   float* ws;                   // [grid][256] cross-CTA partials (slot = contributing CTA)
   int* counters;               // [RT], zero between launches (self-resetting)
@@ -99,6 +107,7 @@ int gemv_smem_bytes(int nwarps);
 
 cudaError_t launch_rht(const RhtParams& p, bool pdl, cudaStream_t s);
 cudaError_t launch_zero(const RhtParams& p, int grid, bool pdl, cudaStream_t s);   // only the n_zero/zero_* fields
+cudaError_t launch_peer_wait(unsigned* flags_local, int world, cudaStream_t s);
 cudaError_t launch_gather_permute(const void* src, void* dst, int world, int batch, int m, int elem_bytes,
                                   cudaStream_t s);
 void count_launch();

@@ -182,6 +182,30 @@ __global__ void qp_gather_permute_kernel(const uint8_t* __restrict__ src, uint8_
   }
 }
 
+// Fused all-gather completion on this rank: flags_local[q] counts the launches rank q has
+// completed into our y_full; flags_local[world] is how many we have consumed. Waits until every
+// rank is one ahead, then consumes (graph-replay safe: no host-side epoch).
+__global__ void qp_peer_wait_kernel(unsigned* flags_local, int world) {
+  if (threadIdx.x != 0) return;
+  const unsigned want = flags_local[world] + 1u;
+  for (int q = 0; q < world; ++q) {
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags_local + q) : "memory");
+      if ((int)(v - want) >= 0) break;
+      __nanosleep(64);
+    }
+  }
+  flags_local[world] = want;
+  __threadfence_system();
+}
+
+cudaError_t launch_peer_wait(unsigned* flags_local, int world, cudaStream_t s) {
+  qp_peer_wait_kernel<<<1, 32, 0, s>>>(flags_local, world);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gather_permute(const void* src, void* dst, int world, int batch, int m, int eb, cudaStream_t s) {
   const long long n = (long long)world * batch * m;
   int grid = (int)((n + 255) / 256);

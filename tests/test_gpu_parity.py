@@ -496,3 +496,34 @@ def test_torch_caching_allocator_backs_layers():
         del lay
     finally:
         Lb.use_torch_allocator(False)
+
+
+@pytest.mark.parametrize("batch,y_dtype", [(1, torch.float32), (3, torch.float16), (8, torch.float32)])
+def test_fused_allgather_p2p_world1(batch, y_dtype):
+    """qp_linear_fwd_sharded_p2p (NEXT-2) at world size 1: the epilogue's direct stores into the
+    (here: own) y_full, the grid-completion signal and the wait kernel. Repeated launches and a
+    CUDA graph check that the counters self-reset / advance (no host-side epoch)."""
+    Lb = _need_gpu()
+    lay, codes, s, ocb = _layer("tcq", 10, 1024, 2048, layer_id=41)
+    x = activations_fp16(batch, 2048)
+    ref = linear.linear_from_codes(codes, 1024, 2048, "tcq", 10, ocb, s, x.astype(np.float64), SEED)
+    shard = lay.shard(0, 1)
+    pg = Lb.PeerGather(1, 0, 1024, batch, dtype=y_dtype)
+    xg = torch.from_numpy(x).cuda()
+    for _ in range(3):
+        pg.y.zero_()
+        pg.forward(shard, xg)
+        torch.cuda.synchronize()
+        assert np.max(linear.normwise_error(pg.y.float().cpu().numpy(), ref)) <= TOL
+    assert int(pg.flags[1].item()) == 3 and int(pg.flags[0].item()) == 3
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            pg.forward(shard, xg, stream=st)
+        pg.y.zero_()
+        for _ in range(4):
+            g.replay()
+        st.synchronize()
+    assert int(pg.flags[1].item()) == 7
+    assert np.max(linear.normwise_error(pg.y.float().cpu().numpy(), ref)) <= TOL
