@@ -278,7 +278,10 @@ def main():
         bufs.append((xb, yb))
     torch.cuda.synchronize()
 
+    extra_flags = int(os.environ.get("QP_BENCH_FLAGS", "0"))     # experiments only (e.g. 4 = QP_DETERMINISTIC)
+
     def fwd(inst, stream=None, flags=0):
+        flags |= extra_flags
         if world > 1:
             inst["layer"].forward_sharded(inst["x"], batch, inst["y"], comm, flags=flags, stream=stream)
         else:
