@@ -677,6 +677,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
 
   float hp[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};   // head row-tile partial
   uint32_t cur[4 * CMAX];
+  int seg_k0 = kt;                                 // first k tile of the current row-tile segment
   bool y_open = false;                             // XM == 2: the in-kernel zeroing of y is done
   int st = 0;
   uint32_t par = 0;
@@ -769,11 +770,11 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
           } else if (RP == 2 || p.y_atomic) {
             // y was zeroed by the preceding kernel: add this warp's scaled partial straight into it
             // (fire-and-forget RED.ADD.F32; no shared-memory reduction, no barrier). RP = 2 is only
-            // launched for the atomic epilogue.
+            // launched for the atomic epilogue. fp16 y (y_ws): into the fp32 workspace instead.
             int i = 0;
 #pragma unroll 1
             while (i + 1 < p.n_out && rth >= p.rt_begin[i + 1]) ++i;
-            float* yb = reinterpret_cast<float*>(p.y[i]) + (rth - p.rt_begin[i]) * kTileRows;
+            float* yb = (p.y_ws ? p.yws[i] : reinterpret_cast<float*>(p.y[i])) + (rth - p.rt_begin[i]) * kTileRows;
 #pragma unroll
             for (int m = 0; m < 2; ++m)
 #pragma unroll
@@ -782,6 +783,25 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
                 if (bb < p.batch)
                   atomicAdd(yb + (size_t)bb * p.ldy[i] + row, acc[2 * h + m][r] * sc[4 * h + 2 * m + (r >> 1)]);
               }
+            if (RP == 1 && p.y_ws) {
+              // count the k tiles this warp contributed; the warp that completes the row tile's KT
+              // converts its 32 rows to fp16 (no waiting anywhere)
+              const int nk = kt - seg_k0 + 1;
+              __threadfence();
+              __syncwarp();
+              int last = 0;
+              if (lane == 0) last = atomicAdd(p.counters + rth, nk) + nk == (int)KT;
+              last = __shfl_sync(0xffffffffu, last, 0);
+              if (last) {
+                __threadfence();
+                __half* yh = reinterpret_cast<__half*>(p.y[i]) + (rth - p.rt_begin[i]) * kTileRows;
+                for (int e = lane; e < kTileRows * p.batch; e += 32) {
+                  const int bb = e / kTileRows, row = e - bb * kTileRows;
+                  yh[(size_t)bb * p.ldy[i] + row] = __float2half_rn(__ldcg(yb + (size_t)bb * p.ldy[i] + row));
+                }
+                if (lane == 0) p.counters[rth] = 0;      // self-reset for the next launch
+              }
+            }
           } else if (t + 1 < b) {
             // partial of a row tile shared with other warps / CTAs, kept in registers until every
             // warp has left the main loop (the partial slots alias x' and the code rings). Only the
@@ -800,6 +820,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
             for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
         }
         if (t + 1 < b) load_scales(rt_n);
+        seg_k0 = 0;                                 // the next segment starts at k tile 0
       }
     }
     kt = kt_n; rt = rt_n;
@@ -990,7 +1011,7 @@ cudaError_t launch_plan(const GemvParams& prm0, int grid, bool pdl, cudaStream_t
   prm.xs_rs = 0;
   // row pairs only where they measured faster: batch >= rp2_min_batch() (8) with a small decode
   // table (VQ / NUQ / UNIF), whose ring keeps >= 2 stages of two tiles
-  if (!DEQ && prm.y_atomic && prm.batch >= rp2_min_batch() && prm.RT % 2 == 0 && PL::TAB <= 32768 &&
+  if (!DEQ && prm.y_atomic && !prm.y_ws && prm.batch >= rp2_min_batch() && prm.RT % 2 == 0 && PL::TAB <= 32768 &&
       PL::AVAIL >= PL::NWARP * 2 * 2 * PL::STAGE) {
     prm.ns = (std::min)(4, PL::AVAIL / (PL::NWARP * 2 * PL::STAGE));
     const int units = (prm.RT / 2) * prm.KT;

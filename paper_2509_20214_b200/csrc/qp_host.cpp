@@ -78,6 +78,15 @@ bool pdl_disabled_by_env() {
   return off;
 }
 
+bool f16_inorder_by_env() {   // QP_F16_INORDER=1: fp16 y through the in-order epilogue (experiments)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QP_F16_INORDER");
+    v = (e && atoi(e) != 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 bool fused_rht_by_env() {   // QP_FUSED_RHT=1: QP_FUSE_RHT on every forward (experiments)
   static int v = -1;
   if (v < 0) {
@@ -186,6 +195,7 @@ struct qp_layer {
   float* d_ws = nullptr;
   int* d_counters = nullptr;
   __half* d_xrot = nullptr;   // [8][d_in] scratch for R x
+  float* d_yws = nullptr;     // [8][d_out] fp32 accumulation workspace for fp16 y
   void* d_gather = nullptr;   // sharded path scratch
   size_t gather_bytes = 0;
 };
@@ -282,7 +292,8 @@ qp_status layer_init(qp_layer* l, int d_out, int d_in, qp_scheme scheme, int bit
   l->d_ws = static_cast<float*>(dev_alloc((size_t)l->grid * 256 * 4));
   l->d_counters = static_cast<int*>(dev_alloc((size_t)(d_out / kTileRows + 2) * 4));   // + grid barrier [2]
   l->d_xrot = static_cast<__half*>(dev_alloc((size_t)8 * d_in * 2));
-  if (!l->d_codes || !l->d_scales || !l->d_ws || !l->d_counters || !l->d_xrot)
+  l->d_yws = static_cast<float*>(dev_alloc((size_t)8 * d_out * 4));
+  if (!l->d_codes || !l->d_scales || !l->d_ws || !l->d_counters || !l->d_xrot || !l->d_yws)
     return fail(QP_ERR_ALLOC, "device allocation of %zu code bytes failed", l->code_bytes);
   CUDA_TRY(cudaMemset(l->d_counters, 0, (size_t)(d_out / kTileRows + 2) * 4), "cudaMemset(counters)");
   return QP_OK;
@@ -295,6 +306,7 @@ void layer_release(qp_layer* l) {
   dev_free(l->d_ws);
   dev_free(l->d_counters);
   dev_free(l->d_xrot);
+  dev_free(l->d_yws);
   dev_free(l->d_gather);
 }
 
@@ -365,6 +377,10 @@ qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, co
                    const FusedRot* fr = nullptr, bool* unsupported = nullptr, bool y_accum = false) {
   GemvParams p{};
   p.y_accum = y_accum ? 1 : 0;
+  if (y_atomic && yt == QP_F16) {                 // fp16 y via the fp32 workspace (zeroed by the caller)
+    p.y_ws = 1;
+    for (int i = 0; i < n_out; ++i) p.yws[i] = l->d_yws + (size_t)batch * rt_begin[i] * kTileRows;
+  }
   if (g_peer_out) {
     p.n_peers = g_peer_out->world;
     for (int k = 0; k < g_peer_out->world; ++k) {
@@ -694,12 +710,15 @@ qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch
   const __half* xr = static_cast<const __half*>(x);
   void* ys[1] = {y};
   // fp32 output: the preceding kernel (rotation, or a zeroing kernel) zeroes y and CTAs that share
-  // a row tile add into it; QP_DETERMINISTIC or fp16 output: in-order cross-CTA reduction instead
-  const bool atomic = yt == QP_F32 && !(flags & QP_DETERMINISTIC);
+  // a row tile add into it; fp16 output: the same into the layer's fp32 workspace, the warp that
+  // completes a row tile converting it; QP_DETERMINISTIC: in-order cross-CTA reduction instead
+  const bool ws16 = yt == QP_F16 && !(flags & QP_DETERMINISTIC) && !g_peer_out && !f16_inorder_by_env();
+  const bool atomic = (yt == QP_F32 && !(flags & QP_DETERMINISTIC)) || ws16;
   const long long zn[1] = {(long long)batch * l->d_out};
   const int rtb[2] = {0, l->d_out / kTileRows};
   const int ldy[1] = {l->d_out};
-  if (!(flags & QP_X_PREROTATED) && ((flags & QP_FUSE_RHT) || fused_rht_by_env())) {
+  void* zs[1] = {ws16 ? static_cast<void*>(l->d_yws) : y};
+  if (!(flags & QP_X_PREROTATED) && !ws16 && ((flags & QP_FUSE_RHT) || fused_rht_by_env())) {
     // one kernel: every CTA rotates x itself (and zeroes y) -- no rotation kernel on the path;
     // falls through to the two-kernel path when x' does not fit the fused plan
     const FusedRot fr{l->rht, x, xt, atomic && !(flags & QP_Y_ACCUMULATE)};
@@ -710,13 +729,13 @@ qp_status qp_linear_fwd(const qp_layer* l, const void* x, qp_dtype xt, int batch
   int side = 0;
   if (!(flags & QP_X_PREROTATED)) {
     const int nz = atomic && !(flags & QP_Y_ACCUMULATE) ? 1 : 0;
-    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, pdl, s, nz, ys, zn)) != QP_OK) return st;
+    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, pdl, s, nz, zs, zn)) != QP_OK) return st;
     xr = l->d_xrot;
     side = batch * (l->d_in / l->rht->block);
   } else if (atomic && !(flags & QP_Y_ACCUMULATE)) {
     RhtParams zp{};
     zp.n_zero = 1;
-    zp.zero_ptr[0] = static_cast<float*>(y);
+    zp.zero_ptr[0] = static_cast<float*>(zs[0]);
     zp.zero_n[0] = zn[0];
     side = zero_ctas(zn, 1);
     cudaError_t e = launch_zero(zp, side, pdl, s);
@@ -805,9 +824,18 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
   const qp_layer* l = g->cat;
   const __half* xr = static_cast<const __half*>(x);
   if (pdl_disabled_by_env()) flags |= QP_NO_PDL;
-  const bool atomic = yt == QP_F32 && !(flags & QP_DETERMINISTIC);
+  const bool ws16 = yt == QP_F16 && !(flags & QP_DETERMINISTIC) && !f16_inorder_by_env();
+  const bool atomic = (yt == QP_F32 && !(flags & QP_DETERMINISTIC)) || ws16;
   long long zn[kMaxGroup];
   for (int i = 0; i < n; ++i) zn[i] = (long long)batch * g->d_outs[i];
+  void* zs[kMaxGroup];
+  {
+    size_t off = 0;
+    for (int i = 0; i < n; ++i) {
+      zs[i] = ws16 ? static_cast<void*>(l->d_yws + off) : ys[i];
+      off += (size_t)batch * g->d_outs[i];
+    }
+  }
   int rtb[kMaxGroup + 1];
   int ldy[kMaxGroup];
   rtb[0] = 0;
@@ -815,7 +843,7 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
     rtb[i + 1] = rtb[i] + g->d_outs[i] / kTileRows;
     ldy[i] = g->d_outs[i];
   }
-  if (!(flags & QP_X_PREROTATED) && ((flags & QP_FUSE_RHT) || fused_rht_by_env())) {
+  if (!(flags & QP_X_PREROTATED) && !ws16 && ((flags & QP_FUSE_RHT) || fused_rht_by_env())) {
     const FusedRot fr{l->rht, x, xt, atomic && !(flags & QP_Y_ACCUMULATE)};
     bool unsup = false;
     st = run_gemv(l, nullptr, batch, n, rtb, ys, ldy, yt, !(flags & QP_NO_PDL), s, atomic, 0, &fr, &unsup,
@@ -825,14 +853,14 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
   int side = 0;
   if (!(flags & QP_X_PREROTATED)) {
     const int nz = atomic && !(flags & QP_Y_ACCUMULATE) ? n : 0;
-    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, !(flags & QP_NO_PDL), s, nz, ys, zn)) != QP_OK) return st;
+    if ((st = run_rht(l->rht, x, xt, batch, l->d_xrot, !(flags & QP_NO_PDL), s, nz, zs, zn)) != QP_OK) return st;
     xr = l->d_xrot;
     side = batch * (l->d_in / l->rht->block);
   } else if (atomic && !(flags & QP_Y_ACCUMULATE)) {
     RhtParams zp{};
     zp.n_zero = n;
     for (int i = 0; i < n; ++i) {
-      zp.zero_ptr[i] = static_cast<float*>(ys[i]);
+      zp.zero_ptr[i] = static_cast<float*>(zs[i]);
       zp.zero_n[i] = zn[i];
     }
     side = zero_ctas(zn, n);

@@ -54,6 +54,10 @@ struct GemvParams {
   int y_f32;                   // 1: fp32 output, 0: fp16 output
   int y_atomic;                // 1: y was zeroed; CTAs sharing a row tile red.add their scaled partials
   int y_accum;                 // 1: QP_Y_ACCUMULATE -- row tiles owned by one warp add into y too
+  // fp16 y through the atomic epilogue: split row tiles red.add into the fp32 workspace yws[i]
+  // (zeroed by the preceding kernel); the warp completing a row tile's k range converts it to y
+  int y_ws;
+  float* yws[kMaxGroup];
   uint32_t zero;               // always 0 (an operand the compiler cannot constant-fold)
   // shared-memory plan chosen at launch (qp_gemv.cuh launch_plan)
   int ns;                      // code-ring stages per warp (1..4)

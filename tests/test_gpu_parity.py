@@ -527,3 +527,37 @@ def test_fused_allgather_p2p_world1(batch, y_dtype):
         st.synchronize()
     assert int(pg.flags[1].item()) == 7
     assert np.max(linear.normwise_error(pg.y.float().cpu().numpy(), ref)) <= TOL
+
+
+@pytest.mark.parametrize("d_out,d_in,scheme,bits_x4,batch", [
+    (4096, 4096, "tcq", 10, 1), (1024, 14336, "half_tcq", 13, 3), (160, 1536, "vq", 12, 8), (512, 2048, "nuq", 16, 2),
+])
+def test_fp16_output_through_workspace(d_out, d_in, scheme, bits_x4, batch):
+    """fp16 y takes the atomic epilogue through the layer's fp32 workspace: split row tiles add into
+    it and the warp completing a row tile's k range converts the tile (per-row-tile counters that
+    self-reset). Same bar as fp32 y; agrees with the in-order (QP_DETERMINISTIC) fp16 path; stable
+    over repeated launches; groups route members' rows."""
+    Lb = _need_gpu()
+    lay, codes, s, ocb = _layer(scheme, bits_x4, d_out, d_in, layer_id=50)
+    x = activations_fp16(batch, d_in)
+    ref = linear.linear_from_codes(codes, d_out, d_in, scheme, bits_x4, ocb, s, x.astype(np.float64), SEED)
+    ys = [_fwd(lay, x, batch, y_dtype=torch.float16) for _ in range(3)]
+    yd = _fwd(lay, x, batch, y_dtype=torch.float16, flags=Lb.QP_DETERMINISTIC)
+    for y in ys + [yd]:
+        assert np.max(linear.normwise_error(y, ref)) <= TOL
+    for y in ys:
+        assert np.max(np.abs(y - yd)) <= 2e-3 * np.max(np.abs(yd))
+    # fused group with fp16 outputs
+    shapes = [(96, 512), (64, 512), (32, 512)]
+    xg = activations_fp16(batch, 512)
+    layers, refs = [], []
+    for i, (do, di) in enumerate(shapes):
+        l2, c2, s2, o2 = _layer(scheme, bits_x4, do, di, layer_id=60 + i)
+        layers.append(l2)
+        refs.append(linear.linear_from_codes(c2, do, di, scheme, bits_x4, o2, s2, xg.astype(np.float64), SEED))
+    g = Lb.Group(layers)
+    outs = [torch.empty(batch, do, device="cuda", dtype=torch.float16) for do, _ in shapes]
+    g.forward(torch.from_numpy(xg).cuda(), batch, outs)
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        assert np.max(linear.normwise_error(o.float().cpu().numpy(), r)) <= TOL
