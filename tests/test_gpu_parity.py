@@ -455,12 +455,12 @@ def test_gpu_trellis_encoder_matches_host_and_oracle(d_out, d_in, scheme, bits_x
     assert abs(dg - do) / do < 1e-6
 
 
-@pytest.mark.parametrize("scheme,bits_x4,paper,tol", [
-    ("tcq", 8, 0.07101, 0.02),    # P:909 Ours-TCQ-2 (L = 16, T = 256, tlut_bits = 9)
-    ("vq", 8, 0.10857, 0.02),     # P:911 Ours-VQ-2 (our k-means codebook: reading R21)
-    ("nuq", 8, 0.11747, 0.005),   # P:910 Ours-NUQ-2
+@pytest.mark.parametrize("scheme,bits_x4,tol", [
+    ("tcq", 8, 0.02),    # P:909 Ours-TCQ-2 (L = 16, T = 256, tlut_bits = 9)
+    ("vq", 8, 0.02),     # P:911 Ours-VQ-2 (our k-means codebook: reading R21)
+    ("nuq", 8, 0.005),   # P:910 Ours-NUQ-2
 ])
-def test_table5_distortion_at_scale(scheme, bits_x4, paper, tol):
+def test_table5_distortion_at_scale(scheme, bits_x4, tol):
     """Table 5 at real scale through the product: a 1024x4096 N(0,1) matrix quantized by
     qp_quantize_offline_gpu (TCQ trellis search on the GPU, L = 16), decoded by qp_dequantize;
     the mean squared error against the oracle's standardized weights W~ matches the paper's
@@ -474,6 +474,8 @@ def test_table5_distortion_at_scale(scheme, bits_x4, paper, tol):
     W_hat = _dequant_gpu(lay).astype(np.float64)
     Wt, _ = linear.gaussianize(W.astype(np.float64), SEED)
     d = float(np.mean((Wt - W_hat) ** 2))
+    from . import golden_values as G
+    paper = G.table5(f"{scheme}-2.0")                 # tests/golden/table5_distortion.json
     assert abs(d - paper) / paper < tol, d
     assert d >= 2.0 ** (-2 * bits_x4 / 4)       # rate-distortion bound
 

@@ -4,6 +4,8 @@ import json
 import os
 
 import numpy as np
+
+from . import golden_values as G  # noqa: E402
 import pytest
 
 from oracle import codebooks as cb
@@ -19,7 +21,7 @@ def test_nuq1_closed_form():
 def test_nuq2_matches_table5():
     # Ours-NUQ-2 mean distortion 0.11747 (std 4.24e-5); Lloyd-Max population optimum 0.117482
     mse = cb.scalar_mse(cb.nuq_lloyd_max(2))
-    assert abs(mse - 0.11747) < 2e-4
+    assert abs(mse - G.table5("nuq-2.0")) < 2e-4
     # textbook Max (1960) 4-level levels +-0.4528, +-1.5104
     assert np.allclose(cb.nuq_lloyd_max(2), [-1.5104, -0.4528, 0.4528, 1.5104], atol=1e-4)
 
@@ -64,9 +66,11 @@ def test_quantlut_sym_traces():
     lut = cb.quantlut_sym(tlut, 16, 9)
     assert lut.shape == (65536, 2)
     assert np.array_equal(lut[0], tlut[0])
-    p, sign, idx = _hash_trace(181)
-    assert (p, sign, idx) == (32942, -1, 2)
-    assert np.array_equal(lut[181], [-tlut[2, 0], tlut[2, 1]])
+    for case in G.load("quantlut_sym_trace.json")["cases"]:
+        w = case["window"]
+        p, sign, idx = _hash_trace(w)
+        assert (p, sign, idx) == (case["p"], case["sign"], case["idx"])
+        assert np.array_equal(lut[w], [case["sign"] * tlut[case["idx"], 0], tlut[case["idx"], 1]])
     for i in np.random.default_rng(1).integers(0, 65536, 200):
         p, sign, idx = _hash_trace(int(i))
         assert np.array_equal(lut[i], [sign * tlut[idx, 0], tlut[idx, 1]])
@@ -142,6 +146,7 @@ def test_frozen_vq2_matches_table5(codebook_dir):
     assert v.shape == (16, 2)
     x = np.random.default_rng(123).standard_normal((1_000_000, 2))
     d = ((x[:, None, :] - v[None]) ** 2).sum(-1).min(1).mean() / 2
-    assert abs(d - 0.10857) / 0.10857 < 0.02        # sklearn Lloyd on 2^20 samples: 0.1075 (-1.0%)
+    ref = G.table5("vq-2.0")
+    assert abs(d - ref) / ref < 0.02        # sklearn Lloyd on 2^20 samples: 0.1075 (-1.0%)
     assert d >= 2.0 ** -4                                   # P:162 bound
     assert d < cb.scalar_mse(cb.nuq_lloyd_max(2))           # Fig. 2 ordering NUQ > VQ

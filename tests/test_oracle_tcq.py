@@ -4,6 +4,8 @@ import itertools
 import os
 
 import numpy as np
+
+from . import golden_values as G  # noqa: E402
 import pytest
 
 from oracle import codebooks as cb
@@ -124,9 +126,9 @@ def test_tcq2_distortion_matches_table5(codebook_dir):
     v = np.random.default_rng(2024).standard_normal((12, 128, 2))
     c, _ = encode.tailbite_rotate_half(v, lut, 4, 16)
     d = c.sum() / v.size
-    assert abs(d - 0.07101) / 0.07101 < 0.06
+    assert abs(d - G.table5("tcq-2.0")) / G.table5("tcq-2.0") < 0.06
     assert d >= 2.0 ** -4                     # no quantizer below 2^(-2b)
-    assert d < 0.10857                        # Fig. 2 / Table 5 ordering: TCQ < VQ < NUQ
+    assert d < G.table5("vq-2.0")             # Fig. 2 / Table 5 ordering: TCQ < VQ < NUQ
 
 
 def test_tcq2_L12_distortion(codebook_dir):
