@@ -227,6 +227,19 @@ int fused_rht_max_rounds() {
   return n;
 }
 
+int ns_cap() {
+  // 2 stages per warp keep the codes NS tiles ahead and leave the rest of shared memory to L1,
+  // where the activations stay resident: up to 12% faster than 3-4 stages for the small-table
+  // schemes, whose rings would otherwise take all of it (profiles/r1/ab_xs_r1.md section 15)
+  static int n = -1;
+  if (n < 0) {
+    const char* e = getenv("QP_NS_MAX");
+    n = e ? atoi(e) : 2;
+    if (n < 1) n = 1;
+  }
+  return n;
+}
+
 int rp2_min_batch() {
   // smallest batch for the row-pair GEMV units (QP_RP2_MIN_BATCH; profiles/r1/ab_xs_r1.md section 9)
   static int n = -1;
