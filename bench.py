@@ -124,6 +124,26 @@ def ncu_traffic(layers, batch):
     return sum(vals) / len(vals), d.get("source")
 
 
+def lib_sha256() -> str:
+    import hashlib
+    with open(os.path.join(ROOT, "paper_2509_20214_b200", "libqpalette.so"), "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
+
+
+def engine_traffic(batch):
+    """DRAM bytes (read + write) per engine launch from the ncu capture in
+    profiles/engine_traffic.json (tools/ncu_traffic.py --engine), used only if that capture was taken
+    with THIS library build (sha256 of libqpalette.so) and this batch; else (None, why)."""
+    p = os.path.join(ROOT, "profiles", "engine_traffic.json")
+    if not os.path.exists(p):
+        return None, "no capture (profiles/engine_traffic.json)"
+    d = json.load(open(p))
+    if d.get("lib_sha256") != lib_sha256():
+        return None, "capture is of another build (lib sha256 differs)"
+    v = d.get("dram_bytes", {}).get(f"b{batch}")
+    return (v, d.get("source")) if v else (None, f"no capture at batch {batch}")
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -205,6 +225,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--path", default="engine", choices=["engine", "layer"],
+                    help="engine: one persistent qp_multi_fwd launch per step (default); layer: qp_linear_fwd "
+                         "per layer (rotation kernel + GEMV kernel each)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -279,6 +302,11 @@ def main():
     torch.cuda.synchronize()
 
     extra_flags = int(os.environ.get("QP_BENCH_FLAGS", "0"))     # experiments only (e.g. 4 = QP_DETERMINISTIC)
+    use_engine = args.path == "engine" and world == 1
+    multis = []
+    if use_engine:
+        for rep in range(REPLICAS):
+            multis.append(QL.Multi([inst["layer"] for inst in insts[rep * n_layers:(rep + 1) * n_layers]]))
 
     def fwd(inst, stream=None, flags=0):
         flags |= extra_flags
@@ -286,6 +314,16 @@ def main():
             inst["layer"].forward_sharded(inst["x"], batch, inst["y"], comm, flags=flags, stream=stream)
         else:
             inst["layer"].forward(inst["x"], batch, inst["y"], flags=flags, stream=stream)
+
+    def step_fn(rep, stream):
+        """One step: the 9 layers of replica `rep` (rotation + fused dequant-GEMV each)."""
+        group = insts[rep * n_layers:(rep + 1) * n_layers]
+        if use_engine:
+            multis[rep].forward([i["x"] for i in group], batch, [i["y"] for i in group], flags=extra_flags,
+                                stream=stream)
+        else:
+            for inst in group:
+                fwd(inst, stream)
 
     # ---- capture one graph per replica ------------------------------------------------
     # (QP_BENCH_EAGER=1 replays the step eagerly instead: ncu cannot profile our kernels inside
@@ -300,13 +338,11 @@ def main():
 
         def replay(self):
             with torch.cuda.stream(stream):
-                for inst in insts[self.rep * n_layers:(self.rep + 1) * n_layers]:
-                    fwd(inst, stream)
+                step_fn(self.rep, stream)
 
     with torch.cuda.stream(stream):
         for rep in range(REPLICAS):
-            for inst in insts[rep * n_layers:(rep + 1) * n_layers]:
-                fwd(inst, stream)          # eager warm-up (sets kernel attributes)
+            step_fn(rep, stream)           # eager warm-up (sets kernel attributes)
         stream.synchronize()
         for rep in range(REPLICAS):
             c0 = QL.launch_count()
@@ -316,8 +352,7 @@ def main():
             else:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
-                    for inst in insts[rep * n_layers:(rep + 1) * n_layers]:
-                        fwd(inst, stream)
+                    step_fn(rep, stream)
             launches_per_step = QL.launch_count() - c0
             graphs.append(g)
     torch.cuda.synchronize()
@@ -417,6 +452,36 @@ def main():
     peak, peak_kind = measured_peaks()
     traffic, traffic_src = ncu_traffic(layers, batch)
 
+    # ---- the engine kernel alone: one CUDA graph of back-to-back qp_multi_fwd launches alternating
+    #      the two replicas (each launch streams 163 MB of codes > L2 126 MB: from HBM), events on
+    #      the launching stream ---------------------------------------------------------------------
+    eng = None
+    eng_traffic, eng_traffic_src = engine_traffic(batch)
+    if use_engine:
+        n_rep = 8
+        with torch.cuda.stream(stream):
+            if eager:
+                def ge_replay():
+                    for k in range(n_rep):
+                        step_fn(k % REPLICAS, stream)
+                ge = type("G", (), {"replay": staticmethod(ge_replay)})
+            else:
+                ge = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(ge, stream=stream):
+                    for k in range(n_rep):
+                        step_fn(k % REPLICAS, stream)
+            for _ in range(3):
+                ge.replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(3, min(args.steps, 30))
+            a.record(stream)
+            for _ in range(reps):
+                ge.replay()
+            b.record(stream)
+            b.synchronize()
+        eng_us = a.elapsed_time(b) * 1e3 / (reps * n_rep)
+        eng = {"achieved": step_bytes / (eng_us * 1e-6) / 1e9, "us": eng_us}
+
     # ---- end to end through the public API with host buffers (N=1 only) ------------------
     # Every step: one H2D copy of the step's 9 activation vectors from pinned host memory, the 9
     # qp_linear_fwd calls, one D2H copy of the 9 results into pinned host memory -- captured with
@@ -432,8 +497,7 @@ def main():
         with torch.cuda.stream(stream):
             def e2e_step(rep):
                 bufs[rep][0].copy_(hx, non_blocking=True)
-                for inst in insts[rep * n_layers:(rep + 1) * n_layers]:
-                    fwd(inst, stream)
+                step_fn(rep, stream)
                 hy.copy_(bufs[rep][1], non_blocking=True)
             for rep in range(REPLICAS):
                 e2e_step(rep)
@@ -486,8 +550,7 @@ def main():
             stream.wait_event(ev_out[r])                # y_r read back (step i-2's D2H done)
             if eager:
                 with torch.cuda.stream(stream):
-                    for inst in insts[r * n_layers:(r + 1) * n_layers]:
-                        fwd(inst, stream)
+                    step_fn(r, stream)
             else:
                 graphs[r].replay()
             ev_comp[r].record(stream)
@@ -538,18 +601,30 @@ def main():
                        "l2": "inputs larger than L2 (2 replicas, 326 MB per 2 steps, L2 126 MB)",
                        "graph": "CUDA graph per step, PDL between consecutive kernels",
                        "kernels_per_layer": round(launches_per_step / n_layers, 3),
-                       "rotation": ("fused into the GEMV kernel (every CTA computes R x in shared memory)"
-                                    if launches_per_step == n_layers else
-                                    "separate rotation kernel before the GEMV kernel"),
+                       "path": ("engine: one persistent qp_multi_fwd launch per step (rotation jobs + all 9 "
+                                "GEMVs, device-side ready flags)" if use_engine else
+                                "per layer: qp_linear_fwd = rotation kernel + fused GEMV kernel, PDL-chained"),
                        "gemv_us_per_layer": per_layer_us},
-            "roofline": {"bound": "hbm", "achieved": round(gemv_achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(gemv_achieved / peak, 4),
-                         "traffic": round(traffic) if traffic else None, "traffic_source": traffic_src,
-                         "algorithmic_bytes_per_launch": round(gemv_alg / n_layers),
-                         "kernel": "qp_gemv_kernel (fused dequant-GEMV), all 9 layers, CUDA graph of back-to-back "
-                                   "launches per layer cycling > 2x L2 of distinct layer copies (codes stream from "
-                                   "HBM), events on the launching stream",
-                         "peak_kind": peak_kind, "avg_launch_us": round(gemv_avg_ms * 1e3, 3)},
+            "roofline": ({"bound": "hbm", "achieved": round(eng["achieved"], 1), "peak": peak, "unit": "GB/s",
+                          "frac": round(eng["achieved"] / peak, 4),
+                          "traffic": round(eng_traffic) if eng_traffic else None, "traffic_source": eng_traffic_src,
+                          "algorithmic_bytes_per_launch": int(step_bytes),
+                          "kernel": "qp_engine_kernel (persistent: the 9 layers' rotations + fused dequant-GEMVs in one "
+                                    "launch), CUDA graph of back-to-back launches alternating 2 replicas of 163 MB of "
+                                    "codes (> L2), events on the launching stream",
+                          "peak_kind": peak_kind, "avg_launch_us": round(eng["us"], 3),
+                          "per_layer_path": {"achieved": round(gemv_achieved, 1), "frac": round(gemv_achieved / peak, 4),
+                                             "avg_launch_us": round(gemv_avg_ms * 1e3, 3),
+                                             "kernel": "qp_gemv_kernel alone per layer (pre-rotated x)"}}
+                         if eng else
+                         {"bound": "hbm", "achieved": round(gemv_achieved, 1), "peak": peak, "unit": "GB/s",
+                          "frac": round(gemv_achieved / peak, 4),
+                          "traffic": round(traffic) if traffic else None, "traffic_source": traffic_src,
+                          "algorithmic_bytes_per_launch": round(gemv_alg / n_layers),
+                          "kernel": "qp_gemv_kernel (fused dequant-GEMV), all 9 layers, CUDA graph of back-to-back "
+                                    "launches per layer cycling > 2x L2 of distinct layer copies (codes stream from "
+                                    "HBM), events on the launching stream",
+                          "peak_kind": peak_kind, "avg_launch_us": round(gemv_avg_ms * 1e3, 3)}),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches_per_step * args.steps),
             "clocks": ck,
         }

@@ -84,6 +84,7 @@ typedef struct qp_codebook qp_codebook;
 typedef struct qp_rht qp_rht;
 typedef struct qp_layer qp_layer;
 typedef struct qp_group qp_group;
+typedef struct qp_multi qp_multi;
 
 /* Route the library's device allocations (e.g. to PyTorch's caching allocator).
  * alloc(size, ctx) returns a device pointer or NULL; free_(ptr, ctx). Pass NULLs to
@@ -99,6 +100,14 @@ qp_status qp_set_allocator(void* (*alloc)(size_t, void*), void (*free_)(void*, v
 qp_status qp_codebook_load(qp_scheme scheme, int bits_x4, int L, const void* host_fp16, size_t n_bytes,
                            qp_codebook** out);
 void qp_codebook_free(qp_codebook* cb);
+
+/* Reconstruction scale alpha of a TCQ codebook at its width (reading R22: "appropriate
+ * scaling", made rate-dependent so that TCQ stays close to the distortion bound at
+ * every width). The frozen tlut keeps unit second moment; the offline quantizers divide
+ * the standardized weights by alpha and store the scales s * alpha, so decode is unchanged.
+ * Values: codebooks/tcq_alpha.json (written by scripts/calibrate_tcq_alpha.py from oracle/).
+ * Default 1. Set it before quantizing. Errors: QP_ERR_INVALID_ARG (NULL, alpha <= 0 / not finite). */
+qp_status qp_codebook_set_scale(qp_codebook* cb, double alpha);
 
 /* Rotation R for inputs of width d_in. block = 0 selects the largest
  * power-of-two divisor of d_in; otherwise block must be a power of two dividing d_in. */
@@ -153,6 +162,28 @@ qp_status qp_fused_linear(const qp_group* g, const void* x, qp_dtype xt, int bat
 /* W_hat[d_out][d_in] (device fp16) without scales: the dequantization-only kernel
  * (P:1154-1163). Bit-exact against the oracle's decode (frozen fp16 codebooks). */
 qp_status qp_dequantize(const qp_layer* l, void* W_hat_fp16, void* stream);
+
+/* Persistent multi-layer engine: y_i = diag(s_i) W_hat_i R_i x_i for a list of n independent
+ * layers (P:345-362 per layer), run as ONE persistent launch per run of consecutive layers that
+ * share a decode table (e.g. TCQ widths 2.5-4.0 on the tb = 9 tlut, or one VQ / NUQ width): the
+ * activation rotations run inside the launch (device-side ready flags instead of a kernel
+ * boundary), the replicated table is built once, every layer's tiles form one stream-K range over
+ * all SMs, and split row tiles reduce through a self-cleaning fp32 workspace (no zeroing kernel).
+ * Layers without an engine variant run through qp_linear_fwd inside qp_multi_fwd.
+ * qp_multi_create references (does not own) the layers: free the qp_multi first. It allocates the
+ * per-layer scratch (x' 16*d_in B, workspace 32*d_out B, counters) once, so qp_multi_fwd never
+ * allocates and is graph-capturable. A qp_multi may be used by one stream at a time.
+ * qp_multi_fwd: xs[i] device [batch][d_in_i] of dtype xt (16-byte aligned; with QP_X_PREROTATED fp16
+ * R x, 32-byte aligned), ys[i] device [batch][d_out_i] of dtype yt in {F16, F32}; outputs must not
+ * alias inputs. Flags: QP_X_PREROTATED, QP_NO_PDL, QP_Y_ACCUMULATE (fp32 y += ...). QP_DETERMINISTIC
+ * and QP_FUSE_RHT are rejected (QP_ERR_INVALID_ARG). Other errors as qp_linear_fwd. */
+qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_multi** out);
+qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype xt, int batch, void* const* ys, qp_dtype yt,
+                       unsigned flags, void* stream);
+/* n_layers; launch groups per qp_multi_fwd (n_launches: one engine launch each, or the per-layer
+ * qp_linear_fwd path for a layer without an engine variant); how many are engine launches. */
+qp_status qp_multi_info(const qp_multi* m, int* n_layers, int* n_launches, int* n_engine_launches);
+void qp_multi_free(qp_multi* m);
 
 /* Contiguous row block [rank*d_out/world, (rank+1)*d_out/world) of a layer as a new
  * layer (device copy). (d_out/world) % 32 must be 0. */

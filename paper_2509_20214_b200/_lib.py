@@ -36,6 +36,7 @@ EXPORTS = [
     "qp_nccl_comm_create", "qp_nccl_comm_destroy", "qp_linear_fwd_sharded", "qp_layer_info", "qp_launch_count",
     "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range", "qp_optimal_bits", "qp_plan_msq",
     "qp_linear_fwd_sharded_p2p", "qp_ipc_handle", "qp_ipc_open", "qp_ipc_close",
+    "qp_codebook_set_scale", "qp_multi_create", "qp_multi_fwd", "qp_multi_info", "qp_multi_free",
 ]
 
 
@@ -59,6 +60,11 @@ def lib() -> C.CDLL:
         sig = {
             "qp_codebook_load": [i, i, i, vp, sz, C.POINTER(vp)],
             "qp_codebook_free": [vp],
+            "qp_codebook_set_scale": [vp, C.c_double],
+            "qp_multi_create": [C.POINTER(vp), i, C.POINTER(vp)],
+            "qp_multi_fwd": [vp, C.POINTER(vp), i, i, C.POINTER(vp), i, C.c_uint, vp],
+            "qp_multi_info": [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i)],
+            "qp_multi_free": [vp],
             "qp_rht_create": [u64, i, i, C.POINTER(vp)],
             "qp_rht_free": [vp],
             "qp_rht_apply": [vp, vp, i, i, vp, vp],
@@ -141,11 +147,19 @@ def shard_range(d_out: int, d_in: int, scheme: str, bits_x4: int, rank: int, wor
 class Codebook:
     """qp_codebook_load: frozen fp16 table (host) -> device decode table."""
 
-    def __init__(self, scheme: str, bits_x4: int, table_fp16: np.ndarray, L: int = 16):
+    def __init__(self, scheme: str, bits_x4: int, table_fp16: np.ndarray, L: int = 16, alpha: float | None = None):
         t = np.ascontiguousarray(table_fp16, dtype="<f2")
         h = C.c_void_p()
         check(lib().qp_codebook_load(SCHEMES[scheme], bits_x4, L, t.ctypes.data, t.nbytes, C.byref(h)))
         self.h, self.scheme, self.bits_x4, self.L = h, scheme, bits_x4, L
+        self.alpha = 1.0
+        if alpha is not None:
+            self.set_scale(alpha)
+
+    def set_scale(self, alpha: float) -> None:
+        """qp_codebook_set_scale: the offline quantizer's reconstruction scale (reading R22)."""
+        check(lib().qp_codebook_set_scale(self.h, float(alpha)))
+        self.alpha = float(alpha)
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
@@ -253,6 +267,34 @@ class Group:
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
             _lib.qp_group_free(self.h)
+            self.h = None
+
+
+class Multi:
+    """qp_multi_*: the persistent multi-layer engine -- one launch runs the rotations and fused
+    dequant-GEMVs of a list of independent layers that share a decode table."""
+
+    def __init__(self, layers: list[Layer]):
+        arr = (C.c_void_p * len(layers))(*[l.h for l in layers])
+        h = C.c_void_p()
+        check(lib().qp_multi_create(arr, len(layers), C.byref(h)))
+        self.h = h
+        self.layers = list(layers)
+        n, nl, ne = C.c_int(), C.c_int(), C.c_int()
+        check(lib().qp_multi_info(self.h, C.byref(n), C.byref(nl), C.byref(ne)))
+        self.n_layers, self.n_launches, self.n_engine_launches = n.value, nl.value, ne.value
+
+    def forward(self, xs: list, batch: int, ys: list, flags: int = 0, stream=None) -> None:
+        """y_i = diag(s_i) W_hat_i R_i x_i for every layer i (qp_multi_fwd)."""
+        assert len(xs) == len(ys) == len(self.layers)
+        xa = (C.c_void_p * len(xs))(*[_ptr(x) for x in xs])
+        ya = (C.c_void_p * len(ys))(*[_ptr(y) for y in ys])
+        check(lib().qp_multi_fwd(self.h, xa, _dtype_code(xs[0]), batch, ya, _dtype_code(ys[0]), flags,
+                                 _stream(stream)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.qp_multi_free(self.h)
             self.h = None
 
 

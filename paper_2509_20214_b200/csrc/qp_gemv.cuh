@@ -213,7 +213,17 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   return v;
 }
 
-template <int MODE, int C, int L, int TB, int REPS, bool DEQ, bool XS>
+// 256-bit activation load through L1 (for x' written by the same launch, e.g. the multi-layer
+// engine's in-kernel rotation: no .nc path)
+__device__ __forceinline__ void load_x8_coh(uint32_t* dst, const __half* src) {
+  asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(dst[0]), "=r"(dst[1]), "=r"(dst[2]), "=r"(dst[3]), "=r"(dst[4]), "=r"(dst[5]), "=r"(dst[6]),
+                 "=r"(dst[7])
+               : "l"(src)
+               : "memory");
+}
+
+template <int MODE, int C, int L, int TB, int REPS, bool DEQ, bool XS, bool COH = false>
 __device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, uint32_t mulk, uint32_t* xb,
                                           float (&acc)[2][4],
                                           uint32_t* wout_lane, int ldw_words, const __half* x_hi,
@@ -226,8 +236,13 @@ __device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, u
   }
   if constexpr (!DEQ && !XS) {
     if (x_hi) {
-      load_x8(xb + 16, x_hi);
-      load_x8(xb + 24, x_hi + 16);
+      if constexpr (COH) {
+        load_x8_coh(xb + 16, x_hi);
+        load_x8_coh(xb + 24, x_hi + 16);
+      } else {
+        load_x8(xb + 16, x_hi);
+        load_x8(xb + 24, x_hi + 16);
+      }
     }
   }
   static_for<16>([&](auto KAP) {
@@ -260,8 +275,13 @@ __device__ __forceinline__ void tile_body(const uint32_t* w, uint32_t laneoff, u
     });
     if constexpr (!DEQ && !XS && kap == 7) {
       if (x_next) {
-        load_x8(xb, x_next);
-        load_x8(xb + 8, x_next + 16);
+        if constexpr (COH) {
+          load_x8_coh(xb, x_next);
+          load_x8_coh(xb + 8, x_next + 16);
+        } else {
+          load_x8(xb, x_next);
+          load_x8(xb + 8, x_next + 16);
+        }
       }
     }
   });

@@ -168,6 +168,7 @@ struct qp_codebook {
   int tb;        // tlut bits (TCQ) or scalar code bits (NUQ/UNIF)
   int mode;      // qp::DecMode
   int reps;
+  double alpha = 1.0;           // reconstruction scale of the offline quantizer (reading R22)
   std::vector<uint16_t> host;   // the loaded fp16 table
   uint32_t* d_table = nullptr;  // compact device table (half2 words)
   int table_words = 0;
@@ -1024,6 +1025,20 @@ extern "C" qp_status qp_ipc_close(void* dev_ptr) {
   return QP_OK;
 }
 
+extern "C" qp_status qp_codebook_set_scale(qp_codebook* cb, double alpha) {
+  if (!cb) return fail(QP_ERR_INVALID_ARG, "codebook is NULL");
+  if (!(alpha > 0.0) || !std::isfinite(alpha))
+    return fail(QP_ERR_INVALID_ARG, "alpha=%g must be positive and finite (codebooks/tcq_alpha.json)", alpha);
+  cb->alpha = alpha;
+  return QP_OK;
+}
+
+extern "C" qp_status qp_internal_codebook_alpha(const qp_codebook* cb, double* alpha) {
+  if (!cb || !alpha) return fail(QP_ERR_INVALID_ARG, "NULL argument");
+  *alpha = cb->alpha;
+  return QP_OK;
+}
+
 extern "C" qp_status qp_internal_codebook_info(const qp_codebook* cb, int* L, int* tb, const uint16_t** host,
                                                size_t* n) {
   if (!cb) return fail(QP_ERR_INVALID_ARG, "codebook is NULL");
@@ -1040,5 +1055,213 @@ extern "C" qp_status qp_internal_rht_info(const qp_rht* r, uint64_t* seed, int* 
   *d_in = r->d_in;
   *block = r->block;
   *sign_bits = r->sign_bits.data();
+  return QP_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// persistent multi-layer engine (qp_multi_*; kernel: qp_engine.cuh)
+// ---------------------------------------------------------------------------------------
+struct qp_multi {
+  struct Group {
+    int first = 0, n = 0;
+    EngineLauncher launch = nullptr;   // nullptr: per-layer qp_linear_fwd (no engine variant)
+    unsigned* d_gen = nullptr;         // [2] exit counter, launches completed
+  };
+  std::vector<const qp_layer*> layers;
+  std::vector<Group> groups;
+  std::vector<__half*> d_xr;           // per layer: x' [8][d_in]
+  std::vector<float*> d_ws;            // per layer: [8][d_out] fp32, zero between launches
+  std::vector<int*> d_cnt;             // per layer: [RT] k-tile counters, zero between launches
+  unsigned* d_flags = nullptr;         // per layer: job_count, ready
+  unsigned* d_gens = nullptr;          // per group [2]
+};
+
+namespace {
+bool same_table(const qp_codebook* a, const qp_codebook* b) {
+  return a == b || (a->mode == b->mode && a->L == b->L && a->tb == b->tb && a->reps == b->reps &&
+                    a->table_words == b->table_words && a->host == b->host);
+}
+double eng_job_tiles() {   // QP_ENG_JOB_TILES: tiles of GEMV work one rotation job displaces
+  static double v = -1;
+  if (v < 0) {
+    const char* e = getenv("QP_ENG_JOB_TILES");
+    v = e ? atof(e) : 8.0;
+  }
+  return v;
+}
+void multi_release(qp_multi* m) {
+  for (auto p : m->d_xr) dev_free(p);
+  for (auto p : m->d_ws) dev_free(p);
+  for (auto p : m->d_cnt) dev_free(p);
+  dev_free(m->d_flags);
+  dev_free(m->d_gens);
+}
+}  // namespace
+
+extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_multi** out) {
+  if (!layers || !out || n < 1) return fail(QP_ERR_INVALID_ARG, "bad arguments to qp_multi_create");
+  *out = nullptr;
+  for (int i = 0; i < n; ++i)
+    if (!layers[i]) return fail(QP_ERR_INVALID_ARG, "layer %d is NULL", i);
+  auto m = new qp_multi();
+  m->layers.assign(layers, layers + n);
+  // consecutive layers sharing a decode table (and an engine variant covering their step widths)
+  // form one persistent launch; at most kMaxEngOps layers each
+  for (int i = 0; i < n;) {
+    qp_multi::Group gr;
+    gr.first = i;
+    int cmin = layers[i]->c_lo, cmax = layers[i]->c_hi;
+    const qp_codebook* cb = layers[i]->cb;
+    EngineLauncher f = find_engine(cb->mode, cb->mode == DEC_LUT2 || cb->mode == DEC_SCALAR ? 0 : cb->L,
+                                   cb->mode == DEC_LUT2 ? 0 : cb->tb, cb->reps, cmin, cmax);
+    int j = i + 1;
+    if (f) {
+      while (j < n && j - i < kMaxEngOps && same_table(layers[j]->cb, cb)) {
+        const int lo = std::min(cmin, layers[j]->c_lo), hi = std::max(cmax, layers[j]->c_hi);
+        EngineLauncher f2 = find_engine(cb->mode, cb->mode == DEC_LUT2 || cb->mode == DEC_SCALAR ? 0 : cb->L,
+                                        cb->mode == DEC_LUT2 ? 0 : cb->tb, cb->reps, lo, hi);
+        if (!f2) break;
+        f = f2;
+        cmin = lo;
+        cmax = hi;
+        ++j;
+      }
+    }
+    gr.n = j - i;
+    gr.launch = f;
+    m->groups.push_back(gr);
+    i = j;
+  }
+  m->d_flags = static_cast<unsigned*>(dev_alloc((size_t)2 * n * 4));
+  m->d_gens = static_cast<unsigned*>(dev_alloc(m->groups.size() * 2 * 4));
+  bool ok = m->d_flags && m->d_gens;
+  for (int i = 0; i < n && ok; ++i) {
+    const qp_layer* l = layers[i];
+    m->d_xr.push_back(static_cast<__half*>(dev_alloc((size_t)8 * l->d_in * 2)));
+    m->d_ws.push_back(static_cast<float*>(dev_alloc((size_t)8 * l->d_out * 4)));
+    m->d_cnt.push_back(static_cast<int*>(dev_alloc((size_t)(l->d_out / kTileRows) * 4)));
+    ok = m->d_xr.back() && m->d_ws.back() && m->d_cnt.back();
+    if (ok && (cudaMemset(m->d_ws.back(), 0, (size_t)8 * l->d_out * 4) != cudaSuccess ||
+               cudaMemset(m->d_cnt.back(), 0, (size_t)(l->d_out / kTileRows) * 4) != cudaSuccess))
+      ok = false;
+  }
+  if (ok && (cudaMemset(m->d_flags, 0, (size_t)2 * n * 4) != cudaSuccess ||
+             cudaMemset(m->d_gens, 0, m->groups.size() * 2 * 4) != cudaSuccess))
+    ok = false;
+  // the memsets run on the legacy stream: complete them before any stream uses the object
+  if (ok && cudaDeviceSynchronize() != cudaSuccess) ok = false;
+  if (!ok) {
+    multi_release(m);
+    delete m;
+    return fail(QP_ERR_ALLOC, "qp_multi_create: device allocation failed");
+  }
+  for (size_t k = 0; k < m->groups.size(); ++k) m->groups[k].d_gen = m->d_gens + 2 * k;
+  *out = m;
+  return QP_OK;
+}
+
+extern "C" void qp_multi_free(qp_multi* m) {
+  if (!m) return;
+  multi_release(m);
+  delete m;
+}
+
+extern "C" qp_status qp_multi_info(const qp_multi* m, int* n_layers, int* n_launches, int* n_engine_launches) {
+  if (!m) return fail(QP_ERR_INVALID_ARG, "NULL qp_multi");
+  if (n_layers) *n_layers = (int)m->layers.size();
+  if (n_launches) *n_launches = (int)m->groups.size();
+  if (n_engine_launches) {
+    int k = 0;
+    for (const auto& g : m->groups) k += g.launch ? 1 : 0;
+    *n_engine_launches = k;
+  }
+  return QP_OK;
+}
+
+extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype xt, int batch, void* const* ys,
+                                  qp_dtype yt, unsigned flags, void* stream) {
+  if (!m || !xs || !ys) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_multi_fwd");
+  const int n = (int)m->layers.size();
+  for (int i = 0; i < n; ++i) {
+    if (!ys[i]) return fail(QP_ERR_INVALID_ARG, "ys[%d] is NULL", i);
+    qp_status st = check_fwd_args(xs[i], xt, batch, yt, flags);
+    if (st != QP_OK) return st;
+    if (!(flags & QP_X_PREROTATED) && (reinterpret_cast<uintptr_t>(xs[i]) & 15u))
+      return fail(QP_ERR_INVALID_ARG, "xs[%d] must be 16-byte aligned (vector loads of the rotation)", i);
+  }
+  if (flags & (QP_DETERMINISTIC | QP_FUSE_RHT))
+    return fail(QP_ERR_INVALID_ARG, "qp_multi_fwd: QP_DETERMINISTIC / QP_FUSE_RHT are per-layer options (use "
+                "qp_linear_fwd)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool pdl = !(flags & QP_NO_PDL) && !pdl_disabled_by_env();
+  const bool pre = (flags & QP_X_PREROTATED) != 0;
+  for (const auto& gr : m->groups) {
+    if (!gr.launch) {
+      for (int i = gr.first; i < gr.first + gr.n; ++i) {
+        qp_status st = qp_linear_fwd(m->layers[i], xs[i], xt, batch, ys[i], yt, flags, stream);
+        if (st != QP_OK) return st;
+      }
+      continue;
+    }
+    static thread_local EngParams p;   // ~6 KB: not on the stack
+    std::memset(&p, 0, sizeof p);
+    p.n_ops = gr.n;
+    p.batch = batch;
+    p.x_dtype = (int)xt;
+    p.y_f32 = yt == QP_F32 ? 1 : 0;
+    p.y_accum = (flags & QP_Y_ACCUMULATE) ? 1 : 0;
+    p.table = m->layers[gr.first]->cb->d_table;
+    p.gen = gr.d_gen;
+    uint32_t tiles = 0;
+    int jobs = 0, scratch = 0;
+    for (int k = 0; k < gr.n; ++k) {
+      const int i = gr.first + k;
+      const qp_layer* l = m->layers[i];
+      EngOp& o = p.op[k];
+      o.codes = l->d_codes;
+      o.scales = l->d_scales;
+      o.RT = l->d_out / kTileRows;
+      o.KT = l->d_in / kTileCols;
+      o.KH = o.KT / 2;
+      o.c_lo = l->c_lo;
+      o.c_hi = l->c_hi;
+      o.rowtile_bytes = (long long)o.KH * 512 * o.c_lo + (long long)(o.KT - o.KH) * 512 * o.c_hi;
+      o.d_in = l->d_in;
+      o.d_out = l->d_out;
+      o.tile0 = tiles;
+      tiles += (uint32_t)(o.RT * o.KT);
+      o.x_raw = xs[i];
+      o.xr = pre ? static_cast<__half*>(const_cast<void*>(xs[i])) : m->d_xr[i];
+      o.rht_signs = l->rht->d_signs;
+      o.rht_block = l->rht->block;
+      o.rht_scale = (float)(1.0 / std::sqrt((double)l->rht->block));
+      o.job0 = jobs;
+      o.njobs = pre ? 0 : batch * (l->d_in / l->rht->block);
+      jobs += o.njobs;
+      if (o.njobs) scratch = std::max(scratch, l->rht->block * 4);
+      o.job_count = m->d_flags + 2 * i;
+      o.ready = m->d_flags + 2 * i + 1;
+      o.y = ys[i];
+      o.ws = m->d_ws[i];
+      o.counters = m->d_cnt[i];
+    }
+    p.total_jobs = jobs;
+    p.rot_scratch_bytes = scratch;
+    const int grid = (int)std::min<long long>(std::min(num_sms(), kMaxEngCtas), tiles);
+    // CTA ranges: the CTAs that run rotation jobs take job_tiles fewer tiles per job
+    const double jt = eng_job_tiles();
+    const double base = ((double)tiles + jt * jobs) / grid;
+    double acc = 0;
+    p.cta_begin[0] = 0;
+    for (int c = 0; c < grid; ++c) {
+      const int my_jobs = c < jobs ? (jobs - 1 - c) / grid + 1 : 0;
+      acc += std::max(0.0, base - jt * my_jobs);
+      p.cta_begin[c + 1] = (uint32_t)std::min<double>(tiles, std::llround(acc));
+    }
+    p.cta_begin[grid] = tiles;
+    cudaError_t e = gr.launch(p, grid, pdl, s);
+    if (e != cudaSuccess) return cuda_fail(e, "engine launch");
+    count_launch();
+  }
   return QP_OK;
 }

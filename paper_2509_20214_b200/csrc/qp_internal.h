@@ -101,6 +101,61 @@ struct RhtParams {
   long long zero_n[kMaxGroup];
 };
 
+// ---- persistent multi-layer engine (qp_engine.cuh, qp_multi_fwd) -----------------------------
+constexpr int kMaxEngOps = 16;      // layers per engine launch
+constexpr int kMaxEngCtas = 192;    // persistent CTAs (>= the SM count)
+
+// One layer of an engine launch. Device pointers into the layer / the qp_multi object.
+struct EngOp {
+  const uint8_t* codes;        // LAYOUT.md stream of the layer
+  const float* scales;         // [d_out]
+  long long rowtile_bytes;     // bytes of one row tile's codes
+  int RT, KT, KH;              // row tiles, k tiles, k tiles at c_lo
+  int c_lo, c_hi;              // bits per step
+  int d_in, d_out;
+  uint32_t tile0;              // first engine-wide tile index of this layer (prefix sum)
+  // rotation: njobs = batch * d_in / rht_block jobs [job0, job0 + njobs), or 0 when x
+  // is already x' (xr = x)
+  const void* x_raw;
+  __half* xr;                  // x' [batch][d_in] fp16
+  const uint32_t* rht_signs;
+  float rht_scale;
+  int rht_block;
+  int job0, njobs;
+  unsigned* job_count;         // jobs finished this launch (reset by the last one)
+  unsigned* ready;             // launches whose x' is complete (monotonic)
+  // outputs: y [batch][d_out]; split row tiles through ws [batch][d_out] fp32 (all zero between
+  // launches) + counters [RT] (k tiles accumulated; zero between launches)
+  void* y;
+  float* ws;
+  int* counters;
+};
+
+struct EngParams {
+  int n_ops, batch;
+  int x_dtype;                 // 0 f16, 1 bf16, 2 f32 (raw x of the rotation jobs)
+  int y_f32, y_accum;
+  int total_jobs;
+  int ns;                      // ring stages per warp (set by the launcher)
+  int rot_scratch_bytes;       // shared memory the rotation jobs need (b_max * 4)
+  uint32_t zero;               // always 0 (an operand the compiler cannot fold)
+  const uint32_t* table;       // compact decode table shared by every layer
+  unsigned* gen;               // [2]: CTAs out this launch, launches completed
+  uint32_t cta_begin[kMaxEngCtas + 1];
+  EngOp op[kMaxEngOps];
+};
+
+struct EngineKey {
+  int mode, L, tb, reps, cmin, cmax;
+  bool operator==(const EngineKey& o) const {
+    return mode == o.mode && L == o.L && tb == o.tb && reps == o.reps && cmin == o.cmin && cmax == o.cmax;
+  }
+};
+using EngineLauncher = cudaError_t (*)(const EngParams&, int grid, bool pdl, cudaStream_t s);
+void register_engine(const EngineKey& k, EngineLauncher f);
+// smallest registered variant of (mode, L, tb, reps) whose c range covers [cmin, cmax]
+EngineLauncher find_engine(int mode, int L, int tb, int reps, int cmin, int cmax);
+
 using GemvLauncher = cudaError_t (*)(const GemvParams&, int grid, int nwarps, bool dequant, bool pdl,
                                      cudaStream_t s);
 

@@ -198,6 +198,7 @@ extern "C" qp_status qp_quantize_offline_gpu(const float* W_host, int d_out, int
 extern "C" {
 qp_status qp_internal_codebook_info(const qp_codebook* cb, int* L, int* tb, const uint16_t** host, size_t* n);
 qp_status qp_internal_rht_info(const qp_rht* r, uint64_t* seed, int* d_in, int* block, const uint32_t** sign_bits);
+qp_status qp_internal_codebook_alpha(const qp_codebook* cb, double* alpha);
 }
 
 static qp_status quantize_offline_impl(const float* W_host, int d_out, int d_in, qp_scheme scheme, int bits_x4,
@@ -213,6 +214,8 @@ static qp_status quantize_offline_impl(const float* W_host, int d_out, int d_in,
   qp_status st = qp_internal_codebook_info(cb, &L, &tb, &host, &nh);
   if (st != QP_OK) return st;
   if ((st = qp_internal_rht_info(r, &seed, &rd_in, &block, &sign_bits)) != QP_OK) return st;
+  double alpha = 1.0;   // reconstruction scale (reading R22): W~ = W' / (s alpha), stored scale s alpha
+  if ((st = qp_internal_codebook_alpha(cb, &alpha)) != QP_OK) return st;
   if (rd_in != d_in) return QP_ERR_CONFIG_MISMATCH;
   if (d_out <= 0 || d_in <= 0 || d_out % 32 || d_in % 256) return QP_ERR_PARTITION_MISMATCH;
   if (n_threads <= 0) n_threads = (int)std::max(1u, std::thread::hardware_concurrency());
@@ -234,7 +237,7 @@ static qp_status quantize_offline_impl(const float* W_host, int d_out, int d_in,
         row[i] *= inv;
         ss += row[i] * row[i];
       }
-      double sc = std::sqrt(ss / d_in);
+      double sc = std::sqrt(ss / d_in) * alpha;
       scales[j] = (float)sc;
       const double is = sc > 0 ? 1.0 / sc : 0.0;
       for (int i = 0; i < d_in; ++i) row[i] *= is;

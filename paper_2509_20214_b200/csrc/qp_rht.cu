@@ -236,6 +236,7 @@ int ns_cap() {
     const char* e = getenv("QP_NS_MAX");
     n = e ? atoi(e) : 2;
     if (n < 1) n = 1;
+    if (n > 4) n = 4;   // the mbarrier area holds 16 warps x 4 stages (1024 B)
   }
   return n;
 }
@@ -287,6 +288,32 @@ GemvLauncher find_gemv(const KernelKey& k) {
   for (const auto& e : registry())
     if (e.k == k) return e.f;
   return nullptr;
+}
+
+namespace {
+struct EngEntry {
+  EngineKey k;
+  EngineLauncher f;
+};
+std::vector<EngEntry>& eng_registry() {
+  static std::vector<EngEntry> r;
+  return r;
+}
+}  // namespace
+
+void register_engine(const EngineKey& k, EngineLauncher f) {
+  std::lock_guard<std::mutex> g(registry_mu());
+  eng_registry().push_back({k, f});
+}
+
+EngineLauncher find_engine(int mode, int L, int tb, int reps, int cmin, int cmax) {
+  std::lock_guard<std::mutex> g(registry_mu());
+  const EngEntry* best = nullptr;
+  for (const auto& e : eng_registry())
+    if (e.k.mode == mode && e.k.L == L && e.k.tb == tb && e.k.reps == reps && e.k.cmin <= cmin && e.k.cmax >= cmax &&
+        (!best || e.k.cmax - e.k.cmin < best->k.cmax - best->k.cmin))
+      best = &e;
+  return best ? best->f : nullptr;
 }
 
 }  // namespace qp

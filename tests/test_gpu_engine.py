@@ -1,0 +1,238 @@
+"""GPU parity of the persistent multi-layer engine (qp_multi_fwd) and of the full-size C2 layers.
+
+Bars as tests/test_gpu_parity.py: y within 2e-3 normwise of the float64 oracle (reading R16) on
+the same seeded inputs, for every layer of an engine launch; the engine's rotation is bitwise the
+rotation kernel's (same operations in the same order), so engine and per-layer outputs agree to
+fp32 summation-order noise.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import decode, linear  # noqa: E402
+from qp_synth import activations_fp16, channel_scales, random_code_bytes  # noqa: E402
+
+from . import qp_cases as Q  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+SEED = 7
+
+
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_20214_b200 import _lib as L
+    return L
+
+
+_CB, _RHT = {}, {}
+
+
+def _cb(scheme, bits_x4, L=16):
+    Lb = _lib()
+    key = (scheme, bits_x4, L)
+    if key not in _CB:
+        _CB[key] = (Lb.Codebook(scheme, bits_x4, Q.load_fp16(scheme, bits_x4), L=L), Q.oracle_codebook(scheme, bits_x4, L))
+    return _CB[key]
+
+
+def _rht(d_in):
+    Lb = _lib()
+    if d_in not in _RHT:
+        _RHT[d_in] = Lb.Rht(SEED, d_in)
+    return _RHT[d_in]
+
+
+def _make(specs, first_id=40):
+    """specs: [(d_out, d_in, scheme, bits_x4)] -> (layers, codes, scales, oracle codebooks)."""
+    Lb = _lib()
+    out = []
+    for i, (d_out, d_in, scheme, x4) in enumerate(specs):
+        cb, ocb = _cb(scheme, x4)
+        codes = random_code_bytes(Q.code_bytes(d_out, d_in, scheme, x4), first_id + i)
+        s = channel_scales(d_out, d_in)
+        out.append((Lb.Layer.from_codes(codes, s, d_out, d_in, scheme, x4, cb, _rht(d_in)), codes, s, ocb, scheme, x4))
+    return out
+
+
+def _ref(item, x):
+    lay, codes, s, ocb, scheme, x4 = item
+    return linear.linear_from_codes(codes, lay.d_out, lay.d_in, scheme, x4, ocb, s, x.astype(np.float64), SEED)
+
+
+# several shapes / widths on the tb = 9 table: ragged tile counts, d_in with 1 .. 7 Hadamard blocks
+TB9_MIX = [(160, 1536, "tcq", 10), (96, 1024, "half_tcq", 13), (64, 3584, "tcq", 16), (256, 512, "tcq", 12),
+           (32, 512, "half_tcq", 11), (128, 14336, "tcq", 14)]
+
+
+@pytest.mark.parametrize("batch", [1, 3, 8])
+@pytest.mark.parametrize("y_dtype", [torch.float32, torch.float16])
+def test_engine_tb9_mix_vs_oracle(batch, y_dtype):
+    Lb = _lib()
+    items = _make(TB9_MIX)
+    m = Lb.Multi([it[0] for it in items])
+    assert m.n_launches == 1 and m.n_engine_launches == 1
+    xs_np = [activations_fp16(batch, it[0].d_in, seed=11 + i) for i, it in enumerate(items)]
+    xs = [torch.from_numpy(x).cuda() for x in xs_np]
+    ys = [torch.full((batch, it[0].d_out), float("nan"), dtype=y_dtype, device="cuda") for it in items]
+    n0 = Lb.launch_count()
+    m.forward(xs, batch, ys)
+    torch.cuda.synchronize()
+    assert Lb.launch_count() - n0 == 1                      # the whole path in one launch
+    for it, x, y in zip(items, xs_np, ys):
+        err = np.max(linear.normwise_error(y.float().cpu().numpy(), _ref(it, x)))
+        assert err <= TOL, (it[0].d_out, it[0].d_in, it[4], it[5], err)
+
+
+@pytest.mark.parametrize("x_dtype", [torch.bfloat16, torch.float32])
+def test_engine_input_dtypes_and_prerotated(x_dtype):
+    Lb = _lib()
+    items = _make(TB9_MIX[:4], first_id=60)
+    m = Lb.Multi([it[0] for it in items])
+    batch = 2
+    xs_np = [activations_fp16(batch, it[0].d_in, seed=21 + i) for i, it in enumerate(items)]
+    xs = [torch.from_numpy(x).to("cuda", x_dtype) for x in xs_np]
+    ys = [torch.empty(batch, it[0].d_out, dtype=torch.float32, device="cuda") for it in items]
+    m.forward(xs, batch, ys)
+    # pre-rotated fp16 x' (qp_rht_apply) through the engine: same outputs up to summation order
+    xr = []
+    for it, x in zip(items, xs):
+        t = torch.empty(batch, it[0].d_in, dtype=torch.float16, device="cuda")
+        _rht(it[0].d_in).apply(x, batch, t)
+        xr.append(t)
+    ys2 = [torch.empty_like(y) for y in ys]
+    m.forward(xr, batch, ys2, flags=Lb.QP_X_PREROTATED)
+    torch.cuda.synchronize()
+    for it, x, y, y2 in zip(items, xs, ys, ys2):
+        y_ref = _ref(it, x.float().cpu().numpy())           # the values the kernel received
+        assert np.max(linear.normwise_error(y.cpu().numpy(), y_ref)) <= TOL
+        assert np.max(linear.normwise_error(y2.cpu().numpy(), y.cpu().numpy())) <= 1e-5
+
+
+def test_engine_repeated_launches_graph_and_accumulate():
+    """Self-cleaning workspace, counters, ready flags and the generation counter across many
+    launches (eager and CUDA-graph replays), plus QP_Y_ACCUMULATE and a batch change."""
+    Lb = _lib()
+    items = _make(TB9_MIX, first_id=80)
+    m = Lb.Multi([it[0] for it in items])
+    refs = {}
+    for batch in (4, 1, 8):
+        xs_np = [activations_fp16(batch, it[0].d_in, seed=31 + i) for i, it in enumerate(items)]
+        xs = [torch.from_numpy(x).cuda() for x in xs_np]
+        ys = [torch.empty(batch, it[0].d_out, dtype=torch.float32, device="cuda") for it in items]
+        refs[batch] = [_ref(it, x) for it, x in zip(items, xs_np)]
+        for _ in range(3):
+            m.forward(xs, batch, ys)
+        torch.cuda.synchronize()
+        for y, r in zip(ys, refs[batch]):
+            assert np.max(linear.normwise_error(y.cpu().numpy(), r)) <= TOL
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            m.forward(xs, batch, ys, stream=s)
+            s.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                m.forward(xs, batch, ys, stream=s)
+            for _ in range(5):
+                g.replay()
+        torch.cuda.synchronize()
+        for y, r in zip(ys, refs[batch]):
+            assert np.max(linear.normwise_error(y.cpu().numpy(), r)) <= TOL
+        # accumulate: y = 1 + W x
+        for y in ys:
+            y.fill_(1.0)
+        m.forward(xs, batch, ys, flags=Lb.QP_Y_ACCUMULATE)
+        torch.cuda.synchronize()
+        for y, r in zip(ys, refs[batch]):
+            assert np.max(linear.normwise_error(y.cpu().numpy() - 1.0, r)) <= TOL
+
+
+def test_engine_mixed_tables_and_fallback():
+    """Layers of different decode tables split into several launches (engine where a variant
+    exists: VQ-3, NUQ-4; the per-layer path for UNIF-8 / DEC_SCALAR and TCQ-5.0)."""
+    Lb = _lib()
+    specs = [(160, 1536, "tcq", 10), (96, 1024, "tcq", 16), (128, 2048, "vq", 12), (64, 1024, "vq", 12),
+             (96, 1536, "nuq", 16), (64, 512, "unif", 32), (32, 1024, "tcq", 20), (64, 768, "tcq", 8)]
+    items = _make(specs, first_id=100)
+    m = Lb.Multi([it[0] for it in items])
+    assert m.n_launches == 6 and m.n_engine_launches == 4
+    batch = 3
+    xs_np = [activations_fp16(batch, it[0].d_in, seed=41 + i) for i, it in enumerate(items)]
+    xs = [torch.from_numpy(x).cuda() for x in xs_np]
+    ys = [torch.empty(batch, it[0].d_out, dtype=torch.float32, device="cuda") for it in items]
+    m.forward(xs, batch, ys)
+    m.forward(xs, batch, ys)
+    torch.cuda.synchronize()
+    for it, x, y in zip(items, xs_np, ys):
+        assert np.max(linear.normwise_error(y.cpu().numpy(), _ref(it, x))) <= TOL, (it[4], it[5])
+
+
+def test_engine_errors():
+    Lb = _lib()
+    items = _make(TB9_MIX[:2], first_id=120)
+    m = Lb.Multi([it[0] for it in items])
+    xs = [torch.zeros(1, it[0].d_in, dtype=torch.float16, device="cuda") for it in items]
+    ys = [torch.zeros(1, it[0].d_out, dtype=torch.float32, device="cuda") for it in items]
+    for flags in (Lb.QP_DETERMINISTIC, Lb.QP_FUSE_RHT):
+        with pytest.raises(Lb.QPError) as e:
+            m.forward(xs, 1, ys, flags=flags)
+        assert e.value.status == 1
+    with pytest.raises(Lb.QPError) as e:
+        m.forward(xs, 9, ys)
+    assert e.value.status == 3
+    buf = torch.zeros(1, items[0][0].d_in + 8, dtype=torch.float16, device="cuda")
+    with pytest.raises(Lb.QPError) as e:                      # x not 16-byte aligned
+        m.forward([buf[:, 1:1 + items[0][0].d_in], xs[1]], 1, ys)
+    assert e.value.status == 1
+
+
+# ---- the C2 workload at full size (BASELINE configs[1]): every output element against the oracle ----
+C2 = [(d_out, d_in, s, x4) for d_out, d_in in [(4096, 4096), (14336, 4096), (4096, 14336)]
+      for s, x4 in [("tcq", 10), ("half_tcq", 13), ("tcq", 16)]]
+
+
+@pytest.fixture(scope="module")
+def c2_reference():
+    """The 9 C2 layers (bench.py's shapes and widths, seeded codes) and their float64 oracle
+    outputs for an 8-row activation batch (rows 0..B-1 are the batch-B inputs)."""
+    _lib()
+    items = _make(C2, first_id=200)
+    x8 = [activations_fp16(8, it[0].d_in, seed=51 + i) for i, it in enumerate(items)]
+    refs = []
+    for it, x in zip(items, x8):
+        lay, codes, s, ocb, scheme, x4 = it
+        W = decode.decode_layer(codes, lay.d_out, lay.d_in, scheme, x4, ocb)
+        refs.append(linear.linear_ref(W, s.astype(np.float64), x.astype(np.float64), SEED))
+        del W
+    return items, x8, refs
+
+
+@pytest.mark.parametrize("batch", [1, 8])
+def test_c2_full_size_per_layer_path(c2_reference, batch):
+    items, x8, refs = c2_reference
+    for it, x, r in zip(items, x8, refs):
+        xg = torch.from_numpy(np.ascontiguousarray(x[:batch])).cuda()
+        y = torch.empty(batch, it[0].d_out, dtype=torch.float32, device="cuda")
+        it[0].forward(xg, batch, y)
+        torch.cuda.synchronize()
+        err = np.max(linear.normwise_error(y.cpu().numpy(), r[:batch]))
+        assert err <= TOL, (it[0].d_out, it[0].d_in, it[5], err)
+
+
+@pytest.mark.parametrize("batch", [1, 8])
+@pytest.mark.parametrize("y_dtype", [torch.float32, torch.float16])
+def test_c2_full_size_engine(c2_reference, batch, y_dtype):
+    Lb = _lib()
+    items, x8, refs = c2_reference
+    m = Lb.Multi([it[0] for it in items])
+    assert m.n_launches == 1
+    xs = [torch.from_numpy(np.ascontiguousarray(x[:batch])).cuda() for x in x8]
+    ys = [torch.empty(batch, it[0].d_out, dtype=y_dtype, device="cuda") for it in items]
+    m.forward(xs, batch, ys)
+    m.forward(xs, batch, ys)
+    torch.cuda.synchronize()
+    for it, y, r in zip(items, ys, refs):
+        err = np.max(linear.normwise_error(y.float().cpu().numpy(), r[:batch]))
+        assert err <= TOL, (it[0].d_out, it[0].d_in, it[5], err)

@@ -1,0 +1,106 @@
+"""Time the persistent multi-layer engine on layer sets (experiments; one JSON line per set).
+
+    python tools/engine_ab.py [--sets c2,c2_tcq25,...] [--batch 1] [--iters 20]
+
+Each set: enough replicas of its layers that one graph of back-to-back qp_multi_fwd launches
+streams > 2x L2 of codes; events on the launching stream; reports us per launch, us per layer,
+and the algorithmic GB/s (SURVEY 8(d) bytes incl. the rotation).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+SHAPES = [(4096, 4096), (14336, 4096), (4096, 14336)]
+SETS = {
+    "c2": [(o, i, s, x) for o, i in SHAPES for s, x in [("tcq", 10), ("half_tcq", 13), ("tcq", 16)]],
+    "c2_tcq25": [(o, i, "tcq", 10) for o, i in SHAPES] * 3,
+    "c2_tcq40": [(o, i, "tcq", 16) for o, i in SHAPES] * 3,
+    "c2_half325": [(o, i, "half_tcq", 13) for o, i in SHAPES] * 3,
+    "big_tcq25": [(14336, 4096, "tcq", 10)] * 6,
+    "sq_tcq25": [(4096, 4096, "tcq", 10)] * 9,
+    "vq3": [(o, i, "vq", 12) for o, i in SHAPES] * 3,
+    "nuq4": [(o, i, "nuq", 16) for o, i in SHAPES] * 3,
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sets", default="c2,c2_tcq25,c2_tcq40,c2_half325,big_tcq25,sq_tcq25")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--prerotated", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph (for ncu)")
+    args = ap.parse_args()
+    import torch
+    from paper_2509_20214_b200 import _lib as QL
+    from qp_synth import activations_fp16, channel_scales, random_code_bytes
+    from tests import qp_cases as Q
+    torch.cuda.set_device(0)
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    cbs, rots = {}, {}
+    B = args.batch
+    for name in args.sets.split(","):
+        specs = SETS[name]
+        nbytes = sum(Q.code_bytes(o, i, s, x) for o, i, s, x in specs)
+        n_rep = max(2, -(-2 * l2 // nbytes) + 1)
+        multis, xs, ys = [], [], []
+        alg = 0
+        for o, i, s, x in specs:
+            b = x / 4
+            tb = 9 if (s != "half_tcq" and b <= 4) or (s == "half_tcq" and b + 0.25 <= 4) else 10
+            lut = 4 << tb if s in ("tcq", "half_tcq") else (4 << int(2 * b) if s == "vq" else 2 << int(b))
+            alg += Q.code_bytes(o, i, s, x) + 4 * o + lut + 2 * B * i + 4 * B * o + (0 if args.prerotated else 4 * B * i)
+        for r in range(n_rep):
+            lays = []
+            for k, (o, i, s, x) in enumerate(specs):
+                key = (s, x)
+                if key not in cbs:
+                    cbs[key] = QL.Codebook(s, x, Q.load_fp16(s, x), L=16)
+                if i not in rots:
+                    rots[i] = QL.Rht(7, i)
+                codes = random_code_bytes(Q.code_bytes(o, i, s, x), 500 + 37 * r + k)
+                lays.append(QL.Layer.from_codes(codes, channel_scales(o, i), o, i, s, x, cbs[key], rots[i]))
+            multis.append(QL.Multi(lays))
+            xs.append([torch.from_numpy(activations_fp16(B, i)).cuda() for o, i, s, x in specs])
+            ys.append([torch.empty(B, o, dtype=torch.float32, device="cuda") for o, i, s, x in specs])
+        flags = QL.QP_X_PREROTATED if args.prerotated else 0
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            def run():
+                for r in range(n_rep):
+                    multis[r].forward(xs[r], B, ys[r], flags=flags, stream=st)
+            run()
+            st.synchronize()
+            if args.eager:
+                g = type("G", (), {"replay": staticmethod(run)})
+            else:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    run()
+            for _ in range(3):
+                g.replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            for _ in range(args.iters):
+                g.replay()
+            b.record(st)
+            b.synchronize()
+        us = a.elapsed_time(b) * 1e3 / (args.iters * n_rep)
+        print(json.dumps({"set": name, "batch": B, "layers": len(specs), "us_per_launch": round(us, 2),
+                          "us_per_layer": round(us / len(specs), 3), "gbs": round(alg / (us * 1e-6) / 1e9, 1),
+                          "launches_per_call": multis[0].n_launches, "replicas": n_rep,
+                          "prerotated": args.prerotated}), flush=True)
+        del multis, xs, ys
+        torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
