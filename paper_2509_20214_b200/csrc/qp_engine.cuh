@@ -24,6 +24,21 @@
 
 namespace qp {
 
+// gpu-scope acq_rel / release atomics: with a preceding bar.sync / bar.warp.sync they publish the
+// whole CTA's / warp's earlier writes (cumulativity) without a MEMBAR.SC per thread, whose store
+// acknowledgements take microseconds while the grid's code copies saturate HBM
+__device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -36,7 +51,10 @@ struct EPlan {
   static constexpr int TAB = ENTRIES * REPS * 4 < 4096 ? 4096 : ENTRIES * REPS * 4;
   static constexpr int SMEM_MAX = 232448;
   static constexpr int STAGE = 512 * CMAX;
-  static constexpr int NWARP = CMAX <= 8 ? 16 : 12;
+#ifndef QP_ENG_WARPS
+#define QP_ENG_WARPS 16
+#endif
+  static constexpr int NWARP = CMAX <= 8 ? QP_ENG_WARPS : (QP_ENG_WARPS < 12 ? QP_ENG_WARPS : 12);
   static constexpr int BAR_OFF = TAB;                 // <= 16 warps x 4 stages x 8 B
   static constexpr int RING_OFF = TAB + 1024;
   static constexpr int AVAIL = SMEM_MAX - RING_OFF;
@@ -134,6 +152,14 @@ __device__ __forceinline__ void c_dispatch(int c, F&& f) {
   }
 }
 
+#ifdef QP_ENG_TIMELINE
+// experiment builds only (-DQP_ENG_TIMELINE): globaltimer stamps of warp 0 of every CTA
+__device__ unsigned long long g_eng_tl[kMaxEngCtas][8];
+#define QP_TL(k) do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_eng_tl[blockIdx.x][k] = t_; } } while (0)
+#else
+#define QP_TL(k) do { } while (0)
+#endif
+
 template <int MODE, int L, int TB, int REPS, int CMIN, int CMAX>
 __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 32, 1)
     qp_engine_kernel(const __grid_constant__ EngParams p) {
@@ -144,71 +170,77 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   if (threadIdx.x == 0 && smem_u32(qp_smem) != kDynSmemBase) __trap();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
+  QP_TL(0);
 
   TableBuild<REPS, NWARP * 32, PL::ENTRIES> tbl;
   tbl.load(p.table);
 
-  // ---- this CTA's tiles, and this warp's share --------------------------------------------------
+  // ---- this warp's tiles: [a, b) of the flat order (host-computed CTA ranges, split evenly over
+  //      the CTA's warps) ------------------------------------------------------------------------
   const uint32_t T0 = p.cta_begin[blockIdx.x], T1 = p.cta_begin[blockIdx.x + 1];
   const uint32_t nC = T1 - T0;
   const uint32_t a = T0 + nC * warp / NWARP, b = T0 + nC * (warp + 1) / NWARP;
-  // locate tile a: op oi, row tile rt, k tile kt (once per warp)
+  // packed geometry of a layer: KT | KH << 8 | c_lo << 16 | c_hi << 24 (KT <= 255, c <= 10)
+  auto pack = [&](int o_) -> uint32_t {
+    const EngOp& o = p.op[o_];
+    return (uint32_t)o.KT | ((uint32_t)o.KH << 8) | ((uint32_t)o.c_lo << 16) | ((uint32_t)o.c_hi << 24);
+  };
+  // decode cursor of tile a: layer oi, row tile rt, k tile kt, geometry opk, tiles left in the layer
   int oi = 0;
   while (oi + 1 < p.n_ops && a >= p.op[oi + 1].tile0) ++oi;
-  uint32_t rt, kt;
+  uint32_t rt, kt, opk = 0, left = 0;
   {
-    const uint32_t loc = a - p.op[oi].tile0;
-    rt = loc / (uint32_t)p.op[oi].KT;
-    kt = loc - rt * (uint32_t)p.op[oi].KT;
+    const uint32_t loc = a - p.op[oi].tile0, KT_ = (uint32_t)p.op[oi].KT;
+    rt = loc / KT_;
+    kt = loc - rt * KT_;
+    if (a < b) {
+      opk = pack(oi);
+      left = (uint32_t)p.op[oi].RT * KT_ - loc;
+    }
   }
-  // ---- the code ring + its fetch cursor (runs NS tiles ahead, across layers) -------------------
-  // The cursor lives in shared memory (only lane 0 issues copies), keeping the main loop's
-  // register budget for the decode.
+
+  // ---- the code ring -------------------------------------------------------------------------
   const uint32_t ring = smem_u32(smem + PL::RING_OFF) + (uint32_t)(warp * NS * PL::STAGE);
   const uint32_t bars = smem_u32(smem + PL::BAR_OFF) + (uint32_t)(warp * NS * 8);
-  struct FCur {
-    const uint8_t* ptr;   // next tile to fetch
-    int oi, kt;           // its layer and k tile
-    uint32_t left;        // tiles left in layer oi (from ptr on)
-    int pad;
-  };
-  static_assert(sizeof(FCur) == 24, "fetch cursor");
-  FCur* fc = reinterpret_cast<FCur*>(smem + PL::BAR_OFF + 512) + warp;
-  // fetch the cursor's tile into stage st and advance the cursor (lane 0)
-  auto fetch = [&](int st, uint32_t dep) {
-    FCur f = *fc;
-    const EngOp& o = p.op[f.oi];
-    const uint32_t nb = 512u * (uint32_t)(f.kt < o.KH ? o.c_lo : o.c_hi);
-    const uint32_t bar = bars + 8u * st;
-    mbar_expect_tx(bar, nb);
-    bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, f.ptr, nb, bar, l2_evict_first_policy());
-    f.ptr += nb;
-    if (++f.kt == o.KT) f.kt = 0;
-    if (--f.left == 0 && f.oi + 1 < p.n_ops) {
-      ++f.oi;
-      f.ptr = p.op[f.oi].codes;
-      f.kt = 0;
-      f.left = (uint32_t)p.op[f.oi].RT * p.op[f.oi].KT;
+  // Copy the tile d positions after the decode cursor (oi_, rt_, kt_, left_, opk_) into stage st
+  // (lane 0 issues). Warp-uniform address arithmetic, no live fetch cursor: the same row in one
+  // add, a row / layer boundary by a short loop.
+  auto fetch_ahead = [&](int st, uint32_t dep, uint32_t d, int oi_, uint32_t rt_, uint32_t kt_, uint32_t left_,
+                         uint32_t opk_) {
+    if (d < left_ && kt_ + d < (opk_ & 0xffu)) {
+      kt_ += d;
+    } else if (d < left_) {
+      const uint32_t KT_ = opk_ & 0xffu;
+      kt_ += d;
+      while (kt_ >= KT_) { kt_ -= KT_; ++rt_; }
+    } else {                                   // in a later layer
+      d -= left_;
+      ++oi_;
+      while (oi_ + 1 < p.n_ops && d >= (uint32_t)(p.op[oi_].RT * p.op[oi_].KT)) {
+        d -= (uint32_t)(p.op[oi_].RT * p.op[oi_].KT);
+        ++oi_;
+      }
+      opk_ = pack(oi_);
+      rt_ = d / (opk_ & 0xffu);
+      kt_ = d - rt_ * (opk_ & 0xffu);
     }
-    *fc = f;
-  };
-  auto init_cursor = [&]() {
-    const EngOp& o = p.op[oi];
-    FCur f;
-    f.oi = oi;
-    f.kt = (int)kt;
-    f.left = (uint32_t)o.RT * o.KT - (a - o.tile0);
-    f.ptr = o.codes + (long long)rt * o.rowtile_bytes +
-            ((int)kt < o.KH ? (long long)kt * 512 * o.c_lo
-                            : (long long)o.KH * 512 * o.c_lo + (long long)((int)kt - o.KH) * 512 * o.c_hi);
-    f.pad = 0;
-    *fc = f;
+    const EngOp& o = p.op[oi_];
+    const uint32_t KH_ = (opk_ >> 8) & 0xffu, clo = (opk_ >> 16) & 0xffu, chi = opk_ >> 24;
+    const uint8_t* src = o.codes + (long long)rt_ * o.rowtile_bytes +
+                         (kt_ < KH_ ? kt_ * 512u * clo : KH_ * 512u * clo + (kt_ - KH_) * 512u * chi);
+    const uint32_t nb = 512u * (kt_ < KH_ ? clo : chi);
+    if (lane == 0) {
+      const uint32_t bar = bars + 8u * st;
+      mbar_expect_tx(bar, nb);
+      bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, src, nb, bar, l2_evict_first_policy());
+    }
   };
 
   // ---- rotation jobs (the first CTAs): x' of every layer, before this CTA's own tiles ------------
   const bool rotor = (int)blockIdx.x < p.total_jobs;
   if (rotor) {
     asm volatile("griddepcontrol.wait;" ::: "memory");          // x may come from the previous kernel
+    QP_TL(1);
     for (int j = blockIdx.x; j < p.total_jobs; j += gridDim.x) {
       int jo = 0;
       while (jo + 1 < p.n_ops && j >= p.op[jo + 1].job0) ++jo;
@@ -216,15 +248,9 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       const int jl = j - o.job0, nblk = o.d_in / o.rht_block;
       const int beta = jl / nblk, blk = jl - beta * nblk;
       engine_rotate<NWARP>(o, p.x_dtype, beta, blk, reinterpret_cast<float*>(smem));   // table / ring area: not live
-      __threadfence();
+      QP_TL(7);
       __syncthreads();
-      if (tid == 0) {
-        if (atomicAdd(o.job_count, 1u) == (unsigned)(o.njobs - 1)) {   // the layer's last job: x' complete
-          *o.job_count = 0u;
-          __threadfence();
-          atomicAdd(o.ready, 1u);
-        }
-      }
+      if (tid == 0) red_add_release(o.ready, 1u);               // one more of the layer's jobs done
     }
     __syncthreads();                                            // scratch reads done before the table build
   }
@@ -232,28 +258,37 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
 #pragma unroll 1
     for (int st = 0; st < NS; ++st) mbar_init(bars + 8u * st, 1);
     mbar_fence_init();
-    init_cursor();
-    if (a < b) fetch(0, 0u);
   }
+  __syncwarp();
+  if (a < b) fetch_ahead(0, 0u, 0u, oi, rt, kt, left, opk);
+  QP_TL(2);
   tbl.store(smem);
-  if (lane == 0)
-    for (int st = 1; st < NS && a + st < b; ++st) fetch(st, 0u);
+  for (int st = 1; st < NS && a + st < b; ++st) fetch_ahead(st, 0u, (uint32_t)st, oi, rt, kt, left, opk);
   if (!rotor) asm volatile("griddepcontrol.wait;" ::: "memory");
-  // launches of this group completed so far (stable during the launch: bumped by the last CTA out)
-  const unsigned gen = ld_acquire_u32(p.gen + 1);
+  QP_TL(3);
   __syncthreads();
 
   const uint32_t laneoff = (uint32_t)(lane % REPS) * 4u;
   const uint32_t mulk = (1u << (Dec<MODE, CMIN, L, TB, REPS>::KSH > 0 ? Dec<MODE, CMIN, L, TB, REPS>::KSH : 0)) + p.zero;
   const bool xrow = g < p.batch;
-  // x' of op oi for this lane (row g, column group q); the wait for its rotation happens on entry
+  // Register economy: the main loop keeps only a packed copy of the current layer's geometry and
+  // the tiles left in it; every other per-layer field is read from the parameter bank where it is
+  // needed, through an index the compiler cannot hoist (shfl of the layer index), so no per-layer
+  // address set stays live across the decode.
+  auto opaque = [&](int v) -> int { return __shfl_sync(0xffffffffu, v, 0); };
+  // wait until layer o_'s x' is complete in this launch (`ready` counts its finished rotation jobs
+  // and is reset by the last CTA out): relaxed polling, then one acquire
   auto enter_op = [&](int o_) {
     const EngOp& o = p.op[o_];
     if (o.njobs > 0) {
-      for (;;) {
-        if ((int)(ld_acquire_u32(o.ready) - (gen + 1u)) >= 0) break;
-        __nanosleep(64);
+      const unsigned want = (unsigned)o.njobs;
+      if (*reinterpret_cast<volatile const unsigned*>(o.ready) < want) {
+        for (;;) {
+          __nanosleep(32);
+          if (*reinterpret_cast<volatile const unsigned*>(o.ready) >= want) break;
+        }
       }
+      (void)ld_acquire_u32(o.ready);
     }
   };
   float sc[4];
@@ -265,13 +300,14 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   uint32_t xb[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) xb[i] = 0u;
-  // this lane's x' row (g) and column group (q) of layer o_ (recomputed: no live register)
+  // this lane's x' row (g) and column group (q) of layer o_
   auto xlane = [&](int o_) -> const __half* { return p.op[o_].xr + (size_t)g * p.op[o_].d_in + 64 * q; };
   if (a < b) {
     enter_op(oi);
-    const __half* xl = xlane(oi);
+    QP_TL(4);
     load_scales(oi, rt);
     if (xrow) {
+      const __half* xl = xlane(oi);
       load_x8_coh(xb, xl + kt * kTileCols);
       load_x8_coh(xb + 8, xl + kt * kTileCols + 16);
     }
@@ -285,20 +321,15 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   int st = 0;
   uint32_t par = 0;
   for (uint32_t t = a; t < b; ++t) {
-    const EngOp& o = p.op[oi];
+    const uint32_t KT = opk & 0xffu, KH = (opk >> 8) & 0xffu;
     mbar_wait(bars + 8u * st, par);
-    const int c = (int)kt < o.KH ? o.c_lo : o.c_hi;
-    // next tile: same layer -> its first-half activations are loaded mid-tile; else on entry
-    uint32_t kt_n = kt + 1, rt_n = rt;
-    int oi_n = oi;
-    if (kt_n == (uint32_t)o.KT) {
-      kt_n = 0;
-      if (++rt_n == (uint32_t)o.RT) { rt_n = 0; ++oi_n; }
-    }
-    const bool same_op = oi_n == oi;
-    const __half* xl = xlane(oi);
+    const int c = kt < KH ? (int)((opk >> 16) & 0xffu) : (int)(opk >> 24);
+    const bool row_end = kt + 1 == KT;
+    const bool op_end = left == 1u;       // the last tile of this layer
+    // first-half activations of the next tile are loaded mid-tile when it is in the same layer
+    const __half* xl = xlane(opaque(oi));
     const __half* x_hi = xrow ? xl + kt * kTileCols + 32 : nullptr;
-    const __half* x_next = (xrow && t + 1 < b && same_op) ? xl + kt_n * kTileCols : nullptr;
+    const __half* x_next = (xrow && t + 1 < b && !op_end) ? xl + (row_end ? 0u : kt + 1) * kTileCols : nullptr;
     const uint32_t src = ring + (uint32_t)(st * PL::STAGE) + (uint32_t)lane * 16u;
     c_dispatch<CMIN, CMAX>(c, [&](auto CC) {
       constexpr int C = decltype(CC)::value;
@@ -310,15 +341,17 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       }
       // the stage is free once every lane's shared loads have returned (see qp_gemv_kernel)
       const uint32_t dep = __reduce_or_sync(0xffffffffu, cur[4 * C - 1] & p.zero);
-      if (lane == 0 && t + NS < b) fetch(st, dep);
+      if (t + NS < b) fetch_ahead(st, dep, (uint32_t)NS, opaque(oi), rt, kt, left, opk);
       tile_body<MODE, C, L, TB, REPS, false, false, true>(cur, laneoff, mulk, xb, acc, nullptr, 0, x_hi, x_next, 0u);
     });
     if (++st == NS) { st = 0; par ^= 1u; }
 
-    if (kt == (uint32_t)o.KT - 1 || t == b - 1) {
+    if (row_end || t == b - 1) {
       // ---- end of this warp's segment of row tile rt ----
-      const bool own = seg_k0 == 0 && kt == (uint32_t)o.KT - 1;
-      if (own) {
+      const int oe = opaque(oi);
+      const int d_out = p.op[oe].d_out;
+      if (seg_k0 == 0 && row_end) {          // the whole row tile: store directly
+        void* yv = p.op[oe].y;
 #pragma unroll
         for (int m = 0; m < 2; ++m)
 #pragma unroll
@@ -326,47 +359,48 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
             const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
             if (bb < p.batch) {
               const float v = acc[m][r] * sc[2 * m + (r >> 1)];
-              const size_t e = (size_t)bb * o.d_out + rt * kTileRows + row;
+              const size_t e = (size_t)bb * d_out + rt * kTileRows + row;
               if (p.y_f32) {
-                float* y = reinterpret_cast<float*>(o.y) + e;
+                float* y = reinterpret_cast<float*>(yv) + e;
                 *y = p.y_accum ? *y + v : v;
               } else {
-                reinterpret_cast<__half*>(o.y)[e] = __float2half_rn(v);
+                reinterpret_cast<__half*>(yv)[e] = __float2half_rn(v);
               }
             }
           }
       } else {
-        float* wsb = o.ws + rt * kTileRows;
+        float* wsb = p.op[oe].ws + rt * kTileRows;
 #pragma unroll
         for (int m = 0; m < 2; ++m)
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-            if (bb < p.batch) atomicAdd(wsb + (size_t)bb * o.d_out + row, acc[m][r] * sc[2 * m + (r >> 1)]);
+            if (bb < p.batch) atomicAdd(wsb + (size_t)bb * d_out + row, acc[m][r] * sc[2 * m + (r >> 1)]);
           }
         const int nk = (int)kt - seg_k0 + 1;
-        __threadfence();
+        unsigned* cnt = reinterpret_cast<unsigned*>(p.op[oe].counters + rt);
         __syncwarp();
         int done = 0;
-        if (lane == 0) done = atomicAdd(o.counters + rt, nk) + nk == o.KT;
+        if (lane == 0) done = atom_add_acqrel(cnt, (unsigned)nk) + (unsigned)nk == KT;
         done = __shfl_sync(0xffffffffu, done, 0);
         if (done) {
           // every k tile of row tile rt is in the workspace: write y, re-zero the workspace
-          __threadfence();
+          __syncwarp();
+          void* yv = p.op[oe].y;
           for (int e = lane; e < kTileRows * p.batch; e += 32) {
             const int bb = e >> 5, row = e & 31;
-            float* wp = wsb + (size_t)bb * o.d_out + row;
+            float* wp = wsb + (size_t)bb * d_out + row;
             const float v = __ldcg(wp);
             __stcg(wp, 0.f);
-            const size_t ye = (size_t)bb * o.d_out + rt * kTileRows + row;
+            const size_t ye = (size_t)bb * d_out + rt * kTileRows + row;
             if (p.y_f32) {
-              float* y = reinterpret_cast<float*>(o.y) + ye;
+              float* y = reinterpret_cast<float*>(yv) + ye;
               *y = p.y_accum ? *y + v : v;
             } else {
-              reinterpret_cast<__half*>(o.y)[ye] = __float2half_rn(v);
+              reinterpret_cast<__half*>(yv)[ye] = __float2half_rn(v);
             }
           }
-          if (lane == 0) o.counters[rt] = 0;
+          if (lane == 0) st_relaxed(cnt, 0u);
         }
       }
 #pragma unroll
@@ -374,31 +408,43 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
 #pragma unroll
         for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
       seg_k0 = 0;
-      if (t + 1 < b) {
-        if (!same_op) {
-          enter_op(oi_n);
-          const __half* xl = xlane(oi_n);
+    }
+    // ---- advance to the next tile ----
+    --left;
+    if (row_end) {
+      kt = 0;
+      ++rt;
+      if (op_end) {
+        ++oi;
+        rt = 0;
+        if (t + 1 < b) {
+          const int on = opaque(oi);
+          opk = pack(on);
+          left = (uint32_t)p.op[on].RT * p.op[on].KT;
+          enter_op(on);
           if (xrow) {
-            load_x8_coh(xb, xl);
-            load_x8_coh(xb + 8, xl + 16);
+            const __half* xn = xlane(on);
+            load_x8_coh(xb, xn);
+            load_x8_coh(xb + 8, xn + 16);
           }
         }
-        load_scales(oi_n, rt_n);
       }
+      if (t + 1 < b) load_scales(opaque(oi), rt);
+    } else {
+      ++kt;
     }
-    kt = kt_n; rt = rt_n; oi = oi_n;
   }
+  QP_TL(5);
   asm volatile("griddepcontrol.launch_dependents;");
-  // the last CTA out bumps the generation (every CTA read it at entry)
+  // the last CTA out resets the launch's ready counters (every CTA is past its waits)
   __syncthreads();
   if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(p.gen, 1u) == gridDim.x - 1) {
-      *p.gen = 0u;
-      __threadfence();
-      atomicAdd(p.gen + 1, 1u);
+    if (atom_add_acqrel(p.gen, 1u) == gridDim.x - 1) {
+      for (int o_ = 0; o_ < p.n_ops; ++o_) st_relaxed(p.op[o_].ready, 0u);
+      st_relaxed(p.gen, 0u);
     }
   }
+  QP_TL(6);
 }
 
 template <int MODE, int L, int TB, int REPS, int CMIN, int CMAX>

@@ -1072,8 +1072,8 @@ struct qp_multi {
   std::vector<__half*> d_xr;           // per layer: x' [8][d_in]
   std::vector<float*> d_ws;            // per layer: [8][d_out] fp32, zero between launches
   std::vector<int*> d_cnt;             // per layer: [RT] k-tile counters, zero between launches
-  unsigned* d_flags = nullptr;         // per layer: job_count, ready
-  unsigned* d_gens = nullptr;          // per group [2]
+  unsigned* d_flags = nullptr;         // per layer: ready (+ 1 spare word)
+  unsigned* d_gens = nullptr;          // per group [4]
 };
 
 namespace {
@@ -1085,7 +1085,7 @@ double eng_job_tiles() {   // QP_ENG_JOB_TILES: tiles of GEMV work one rotation 
   static double v = -1;
   if (v < 0) {
     const char* e = getenv("QP_ENG_JOB_TILES");
-    v = e ? atof(e) : 8.0;
+    v = e ? atof(e) : 16.0;
   }
   return v;
 }
@@ -1133,7 +1133,7 @@ extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_mu
     i = j;
   }
   m->d_flags = static_cast<unsigned*>(dev_alloc((size_t)2 * n * 4));
-  m->d_gens = static_cast<unsigned*>(dev_alloc(m->groups.size() * 2 * 4));
+  m->d_gens = static_cast<unsigned*>(dev_alloc(m->groups.size() * 4 * 4));
   bool ok = m->d_flags && m->d_gens;
   for (int i = 0; i < n && ok; ++i) {
     const qp_layer* l = layers[i];
@@ -1146,7 +1146,7 @@ extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_mu
       ok = false;
   }
   if (ok && (cudaMemset(m->d_flags, 0, (size_t)2 * n * 4) != cudaSuccess ||
-             cudaMemset(m->d_gens, 0, m->groups.size() * 2 * 4) != cudaSuccess))
+             cudaMemset(m->d_gens, 0, m->groups.size() * 4 * 4) != cudaSuccess))
     ok = false;
   // the memsets run on the legacy stream: complete them before any stream uses the object
   if (ok && cudaDeviceSynchronize() != cudaSuccess) ok = false;
@@ -1155,7 +1155,7 @@ extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_mu
     delete m;
     return fail(QP_ERR_ALLOC, "qp_multi_create: device allocation failed");
   }
-  for (size_t k = 0; k < m->groups.size(); ++k) m->groups[k].d_gen = m->d_gens + 2 * k;
+  for (size_t k = 0; k < m->groups.size(); ++k) m->groups[k].d_gen = m->d_gens + 4 * k;
   *out = m;
   return QP_OK;
 }
@@ -1239,8 +1239,7 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
       o.njobs = pre ? 0 : batch * (l->d_in / l->rht->block);
       jobs += o.njobs;
       if (o.njobs) scratch = std::max(scratch, l->rht->block * 4);
-      o.job_count = m->d_flags + 2 * i;
-      o.ready = m->d_flags + 2 * i + 1;
+      o.ready = m->d_flags + 2 * i;
       o.y = ys[i];
       o.ws = m->d_ws[i];
       o.counters = m->d_cnt[i];
@@ -1248,17 +1247,19 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
     p.total_jobs = jobs;
     p.rot_scratch_bytes = scratch;
     const int grid = (int)std::min<long long>(std::min(num_sms(), kMaxEngCtas), tiles);
-    // CTA ranges: the CTAs that run rotation jobs take job_tiles fewer tiles per job
+    // CTA ranges over the flat tile order; the CTAs that run rotation jobs take job_tiles fewer
+    // tiles per job
+    const uint32_t S = tiles;
     const double jt = eng_job_tiles();
-    const double base = ((double)tiles + jt * jobs) / grid;
+    const double base = ((double)S + jt * jobs) / grid;
     double acc = 0;
     p.cta_begin[0] = 0;
     for (int c = 0; c < grid; ++c) {
       const int my_jobs = c < jobs ? (jobs - 1 - c) / grid + 1 : 0;
       acc += std::max(0.0, base - jt * my_jobs);
-      p.cta_begin[c + 1] = (uint32_t)std::min<double>(tiles, std::llround(acc));
+      p.cta_begin[c + 1] = (uint32_t)std::min<double>(S, std::llround(acc));
     }
-    p.cta_begin[grid] = tiles;
+    p.cta_begin[grid] = S;
     cudaError_t e = gr.launch(p, grid, pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "engine launch");
     count_launch();

@@ -18,4 +18,16 @@ struct Register {
   }
 } register_instance;
 }  // namespace
+
+// experiment builds (-DQP_ENG_TIMELINE): copy the per-CTA stamps of the last engine launch
+extern "C" int qp_debug_engine_timeline(unsigned long long* host, int n) {
+#ifdef QP_ENG_TIMELINE
+  if (n > kMaxEngCtas * 8) n = kMaxEngCtas * 8;
+  return (int)cudaMemcpyFromSymbol(host, g_eng_tl, (size_t)n * 8);
+#else
+  (void)host;
+  (void)n;
+  return -1;
+#endif
+}
 }  // namespace qp

@@ -122,8 +122,7 @@ struct EngOp {
   float rht_scale;
   int rht_block;
   int job0, njobs;
-  unsigned* job_count;         // jobs finished this launch (reset by the last one)
-  unsigned* ready;             // launches whose x' is complete (monotonic)
+  unsigned* ready;             // rotation jobs of this layer finished in this launch (reset at exit)
   // outputs: y [batch][d_out]; split row tiles through ws [batch][d_out] fp32 (all zero between
   // launches) + counters [RT] (k tiles accumulated; zero between launches)
   void* y;
@@ -140,8 +139,8 @@ struct EngParams {
   int rot_scratch_bytes;       // shared memory the rotation jobs need (b_max * 4)
   uint32_t zero;               // always 0 (an operand the compiler cannot fold)
   const uint32_t* table;       // compact decode table shared by every layer
-  unsigned* gen;               // [2]: CTAs out this launch, launches completed
-  uint32_t cta_begin[kMaxEngCtas + 1];
+  unsigned* gen;               // [1]: CTAs out this launch (the last one resets the ready counters)
+  uint32_t cta_begin[kMaxEngCtas + 1];   // CTA c owns tiles [cta_begin[c], cta_begin[c+1])
   EngOp op[kMaxEngOps];
 };
 
