@@ -8,8 +8,10 @@ where W_hat = dq(codes) (oracle/decode.py), R the randomized Hadamard rotation
 (oracle/rht.py) and s the per-output-channel scales. The oracle
 computes it directly in float64.
 
-Offline, data-free weight path (reading R10):
-    W' = W R^T (each row rotated), s_j = RMS(W'_j), W~ = W' / s, codes = encode(W~).
+Offline, data-free weight path (readings R10, R22):
+    W' = W R^T (each row rotated), s_j = RMS(W'_j), W~ = W' / (s alpha), codes = encode(W~),
+    stored scales s alpha (alpha = the codebook's rate-dependent reconstruction scale,
+    oracle/scaling.py; 1 for NUQ / UNIF / VQ).
 """
 from __future__ import annotations
 
@@ -31,17 +33,18 @@ def linear_from_codes(codes, d_out, d_in, scheme, bits_x4, codebook, scales, x, 
     return linear_ref(W_hat, scales, x, seed, prerotated)
 
 
-def gaussianize(W: np.ndarray, seed: int) -> tuple[np.ndarray, np.ndarray]:
-    """W' = W R^T, s_j = sqrt(mean_k W'_jk^2), returns (W' / s, s) (reading R10)."""
+def gaussianize(W: np.ndarray, seed: int, alpha: float = 1.0) -> tuple[np.ndarray, np.ndarray]:
+    """W' = W R^T, s_j = sqrt(mean_k W'_jk^2); returns (W' / (s alpha), s alpha) (readings
+    R10, R22: the quantizer then sees unit-RMS rows shrunk by the reconstruction scale alpha)."""
     Wr = rht.rht_apply(np.asarray(W, dtype=np.float64), seed)     # row j -> R W_j
-    s = np.sqrt(np.mean(Wr * Wr, axis=1))
+    s = np.sqrt(np.mean(Wr * Wr, axis=1)) * alpha
     return Wr / s[:, None], s
 
 
-def quantize_offline(W: np.ndarray, scheme: str, bits_x4: int, codebook: dict, seed: int):
+def quantize_offline(W: np.ndarray, scheme: str, bits_x4: int, codebook: dict, seed: int, alpha: float = 1.0):
     """Data-free quantization of one nn.Linear weight [d_out][d_in].
-    Returns (codes uint8, scales float64)."""
-    Wt, s = gaussianize(W, seed)
+    Returns (codes uint8, scales float64 = s alpha)."""
+    Wt, s = gaussianize(W, seed, alpha)
     return encode.encode_layer(Wt, scheme, bits_x4, codebook), s
 
 

@@ -58,6 +58,17 @@ def oracle_codebook(scheme: str, bits_x4: int, L: int = 16) -> dict:
     return {"lut": t}
 
 
+def tcq_alpha(scheme: str, bits_x4: int, L: int = 16) -> float:
+    """Reconstruction scale alpha of the TCQ / half-TCQ codebook at this width (reading R22,
+    codebooks/tcq_alpha.json, written by scripts/calibrate_tcq_alpha.py from oracle/ only);
+    1 for the other schemes."""
+    if scheme not in ("tcq", "half_tcq"):
+        return 1.0
+    import json
+    d = json.load(open(os.path.join(CB_DIR, "tcq_alpha.json")))
+    return float(d[f"{scheme}/{bits_x4}/L{L}"]["alpha"])
+
+
 def code_bytes(d_out: int, d_in: int, scheme: str, bits_x4: int) -> int:
     from oracle import layout
     return layout.tile_offsets(d_out, d_in, scheme, bits_x4)[1]
