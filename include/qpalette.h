@@ -238,18 +238,30 @@ qp_status qp_linear_fwd_sharded(const qp_layer* shard, const void* x, qp_dtype x
  * {F16, F32}, rank r's rows at columns [r*m, (r+1)*m)); then the grid's last CTA increments this
  * rank's counter in every rank's flag array, and a one-thread wait kernel on `stream` returns once
  * every rank has delivered into this rank's y_full, so later work on `stream` sees the whole
- * vector. y_peers[k] / flag_peers[k]: rank k's y_full and flag array (unsigned[world + 1], zeroed
+ * vector. y_peers[k] / flag_peers[k]: rank k's y_full and flag array (unsigned[2 * world + 1], zeroed
  * once at setup, mapped into this process with qp_ipc_open; this rank's own pointers at k = rank).
+ * Buffer reuse: each call first runs a round-entry barrier (every rank announces the round in all
+ * flag arrays and waits for the others), so a rank stores round n into a peer's y_full only after
+ * that peer has *entered* round n -- i.e. its work on y_full enqueued on `stream` before this call is
+ * done. Readers of y_full must therefore be ordered before the next call on the same stream.
  * Uses the in-order (QP_DETERMINISTIC) epilogue; QP_Y_ACCUMULATE / QP_FUSE_RHT are rejected.
  * Errors: QP_ERR_INVALID_ARG, plus qp_linear_fwd's. Graph-capturable (no host-side epoch). */
 qp_status qp_linear_fwd_sharded_p2p(const qp_layer* shard, const void* x, qp_dtype xt, int batch,
                                     void* const* y_peers, unsigned* const* flag_peers, int rank, int world,
                                     qp_dtype yt, unsigned flags, void* stream);
 
-/* CUDA IPC plumbing for qp_linear_fwd_sharded_p2p: export a device allocation's 64-byte handle,
- * map a peer's handle into this process (peer access enabled lazily), unmap it. */
-qp_status qp_ipc_handle(const void* dev_ptr, void* handle64);
-qp_status qp_ipc_open(const void* handle64, void** dev_ptr);
+/* The permutation qp_linear_fwd_sharded applies after ncclAllGather for batch > 1: src [world][batch][m]
+ * (rank-major, as the all-gather delivers it) -> dst [batch][world * m] (device buffers, elem_bytes 2 or
+ * 4, no aliasing). Exposed for callers that run their own all-gather, and for tests. */
+qp_status qp_gather_permute(const void* src, void* dst, int world, int batch, int m, int elem_bytes, void* stream);
+
+/* CUDA IPC plumbing for qp_linear_fwd_sharded_p2p. qp_ipc_handle writes 72 bytes: the 64-byte CUDA
+ * IPC handle of the allocation that contains dev_ptr (found with cuMemGetAddressRange: dev_ptr may
+ * lie inside a caching-allocator segment) + the 8-byte offset of dev_ptr in it. qp_ipc_open maps a
+ * peer's handle into this process (peer access enabled lazily) and returns the peer's dev_ptr;
+ * qp_ipc_close unmaps it. Errors: QP_ERR_INVALID_ARG (NULL), QP_ERR_CUDA. */
+qp_status qp_ipc_handle(const void* dev_ptr, void* handle72);
+qp_status qp_ipc_open(const void* handle72, void** dev_ptr);
 qp_status qp_ipc_close(void* dev_ptr);
 
 /* Introspection. bits_per_weight counts code bits only (reading R19). */

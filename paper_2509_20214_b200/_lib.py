@@ -36,7 +36,7 @@ EXPORTS = [
     "qp_nccl_comm_create", "qp_nccl_comm_destroy", "qp_linear_fwd_sharded", "qp_layer_info", "qp_launch_count",
     "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range", "qp_optimal_bits", "qp_plan_msq",
     "qp_linear_fwd_sharded_p2p", "qp_ipc_handle", "qp_ipc_open", "qp_ipc_close",
-    "qp_codebook_set_scale", "qp_multi_create", "qp_multi_fwd", "qp_multi_info", "qp_multi_free",
+    "qp_codebook_set_scale", "qp_gather_permute", "qp_multi_create", "qp_multi_fwd", "qp_multi_info", "qp_multi_free",
 ]
 
 
@@ -83,6 +83,7 @@ def lib() -> C.CDLL:
             "qp_set_allocator": [vp, vp, vp],
             "qp_linear_fwd_sharded_p2p": [vp, vp, i, i, vp, vp, i, i, i, C.c_uint, vp],
             "qp_ipc_handle": [vp, vp],
+            "qp_gather_permute": [vp, vp, i, i, i, i, vp],
             "qp_ipc_open": [vp, C.POINTER(vp)],
             "qp_ipc_close": [vp],
             "qp_optimal_bits": [C.POINTER(C.c_double), C.POINTER(C.c_double), i, C.c_double, C.c_double,
@@ -134,6 +135,11 @@ def _stream(stream) -> int:
 def _dtype_code(t) -> int:
     import torch
     return {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2}[t.dtype]
+
+
+def gather_permute(src, dst, world: int, batch: int, m: int, stream=None) -> None:
+    """qp_gather_permute: [world][batch][m] -> [batch][world * m] (device tensors)."""
+    check(lib().qp_gather_permute(_ptr(src), _ptr(dst), world, batch, m, src.element_size(), _stream(stream)))
 
 
 def shard_range(d_out: int, d_in: int, scheme: str, bits_x4: int, rank: int, world: int):
@@ -386,13 +392,13 @@ class PeerGather:
         dtype = dtype or torch.float32
         self.world, self.rank, self.m, self.batch = world, rank, m, batch
         self.y = torch.zeros(batch, world * m, dtype=dtype, device="cuda")
-        self.flags = torch.zeros(world + 1, dtype=torch.int32, device="cuda")
+        self.flags = torch.zeros(2 * world + 1, dtype=torch.int32, device="cuda")   # delivered | consumed | entered
         self._opened = []
         if world == 1:
             ys, fs = [self.y.data_ptr()], [self.flags.data_ptr()]
         else:
             import torch.distributed as dist
-            hy, hf = (C.c_char * 64)(), (C.c_char * 64)()
+            hy, hf = (C.c_char * 72)(), (C.c_char * 72)()
             check(lib().qp_ipc_handle(C.c_void_p(self.y.data_ptr()), hy))
             check(lib().qp_ipc_handle(C.c_void_p(self.flags.data_ptr()), hf))
             allh = [None] * world

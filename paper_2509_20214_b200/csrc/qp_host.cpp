@@ -297,6 +297,9 @@ qp_status layer_init(qp_layer* l, int d_out, int d_in, qp_scheme scheme, int bit
   if (!l->d_codes || !l->d_scales || !l->d_ws || !l->d_counters || !l->d_xrot || !l->d_yws)
     return fail(QP_ERR_ALLOC, "device allocation of %zu code bytes failed", l->code_bytes);
   CUDA_TRY(cudaMemset(l->d_counters, 0, (size_t)(d_out / kTileRows + 2) * 4), "cudaMemset(counters)");
+  // the memset runs on the legacy default stream, which PyTorch's (non-blocking) streams do not
+  // order against: complete it before the layer is handed out
+  CUDA_TRY(cudaStreamSynchronize(0), "cudaStreamSynchronize(layer init)");
   return QP_OK;
 }
 
@@ -421,10 +424,6 @@ qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, co
   p.y_f32 = yt == QP_F32 ? 1 : 0;
   p.ws = l->d_ws;
   p.counters = l->d_counters;
-  static const bool tl = getenv("QP_TIMELINE") != nullptr;
-  static unsigned long long* d_tl = nullptr;
-  if (tl && !d_tl) { cudaMalloc(&d_tl, 4096 * 128 * 8); cudaMemset(d_tl, 0, 4096 * 128 * 8); }
-  p.timeline = tl ? d_tl : nullptr;
   int grid = l->grid;
   if (pdl && side_ctas > 0 && side_ctas <= kMaxSideCtas) grid = std::max(1, std::min(grid, num_sms() - side_ctas));
   set_magics(p, grid);
@@ -435,31 +434,6 @@ qp_status run_gemv(const qp_layer* l, const __half* xr, int batch, int n_out, co
   }
   if (e != cudaSuccess) return cuda_fail(e, "fused dequant-GEMV launch");
   count_launch();
-  if (tl) {
-    std::vector<unsigned long long> h(grid * 128, 0ull);
-    cudaStreamSynchronize(s);
-    cudaMemcpy(h.data(), d_tl, h.size() * 8, cudaMemcpyDeviceToHost);
-    double av[8] = {0}, mx[8] = {0};
-    int cnt[8] = {0};
-    for (int c = 0; c < grid; ++c) {
-      unsigned long long st = ~0ull;
-      for (int w = 0; w < 16; ++w) if (h[(c * 16 + w) * 8]) st = std::min(st, h[(c * 16 + w) * 8]);
-      for (int k = 1; k < 8; ++k) {
-        double m = -1;
-        for (int w = 0; w < 16; ++w) {
-          unsigned long long v = h[(c * 16 + w) * 8 + k];
-          if (v && v > st) m = std::max(m, (double)(v - st) / 1000.0);
-        }
-        if (m >= 0) { av[k] += m; cnt[k]++; mx[k] = std::max(mx[k], m); }
-      }
-    }
-    fprintf(stderr, "kcyc (avg/max over CTAs):");
-    const char* nm[8] = {"", "table", "mainend", "epiend", "epistart", "afterwait", "afterexpand", "afterstage"};
-    for (int k = 1; k < 8; ++k) fprintf(stderr, " %s %.2f/%.2f", nm[k], cnt[k] ? av[k] / cnt[k] : 0.0, mx[k]);
-    fprintf(stderr, " grid %d", grid);
-    fprintf(stderr, "\n");
-    cudaMemset(d_tl, 0, 4096 * 128 * 8);
-  }
   return QP_OK;
 }
 
@@ -800,6 +774,11 @@ qp_status qp_fuse(const qp_layer* const* members, int n, qp_group** out) {
     row += m->d_out;
     g->d_outs.push_back(m->d_out);
   }
+  // device-to-device copies on the legacy stream: complete before the group is used elsewhere
+  if (cudaError_t e = cudaStreamSynchronize(0); e != cudaSuccess) {
+    qp_group_free(g);
+    return cuda_fail(e, "group concatenation");
+  }
   *out = g;
   return QP_OK;
 }
@@ -909,6 +888,18 @@ qp_status qp_layer_shard(const qp_layer* l, int rank, int world, qp_layer** out)
   cudaError_t e = cudaMemcpy(s->d_codes, l->d_codes + byte0, nb, cudaMemcpyDeviceToDevice);
   if (e == cudaSuccess)
     e = cudaMemcpy(s->d_scales, l->d_scales + row0, (size_t)m * 4, cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);   // legacy-stream copies done before use
+  if (e == cudaSuccess) {
+    // the all-gather scratch of qp_linear_fwd_sharded for up to batch 8, fp32: allocated here, so the
+    // forward never allocates (CUDA-graph capture safe)
+    s->gather_bytes = (size_t)(world + 1) * 8 * m * 4;
+    s->d_gather = dev_alloc(s->gather_bytes);
+    if (!s->d_gather) {
+      layer_release(s);
+      delete s;
+      return fail(QP_ERR_ALLOC, "shard all-gather scratch allocation failed");
+    }
+  }
   if (e != cudaSuccess) {
     layer_release(s);
     delete s;
@@ -949,6 +940,9 @@ qp_status qp_linear_fwd_sharded(const qp_layer* shard, const void* x, qp_dtype x
   if (!shard || !y_full || !comm) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_linear_fwd_sharded");
   qp_status st = check_fwd_args(x, xt, batch, yt, flags);
   if (st != QP_OK) return st;
+  if (flags & QP_Y_ACCUMULATE)
+    return fail(QP_ERR_INVALID_ARG, "qp_linear_fwd_sharded: QP_Y_ACCUMULATE is not supported (the all-gather "
+                "overwrites y_full). Remedy: add the residual after the call");
   ncclComm_t c = static_cast<ncclComm_t>(comm);
   int world = 0;
   if (ncclCommCount(c, &world) != ncclSuccess || world < 1) return fail(QP_ERR_NCCL, "ncclCommCount failed");
@@ -957,12 +951,9 @@ qp_status qp_linear_fwd_sharded(const qp_layer* shard, const void* x, qp_dtype x
   const int eb = yt == QP_F32 ? 4 : 2;
   qp_layer* l = const_cast<qp_layer*>(shard);
   const size_t need = (size_t)(world + 1) * batch * m * eb;
-  if (l->gather_bytes < need) {
-    dev_free(l->d_gather);
-    l->d_gather = dev_alloc(need);
-    l->gather_bytes = l->d_gather ? need : 0;
-    if (!l->d_gather) return fail(QP_ERR_ALLOC, "gather scratch allocation failed");
-  }
+  if (l->gather_bytes < need)
+    return fail(QP_ERR_CONFIG_MISMATCH, "qp_linear_fwd_sharded: the layer is not a shard of a %d-rank split "
+                "(qp_layer_shard allocates the all-gather scratch). Remedy: shard with world = %d", world, world);
   uint8_t* local = static_cast<uint8_t*>(l->d_gather);              // [batch][m]
   uint8_t* gathered = local + (size_t)batch * m * eb;                // [world][batch][m]
   if ((st = qp_linear_fwd(shard, x, xt, batch, local, yt, flags, stream)) != QP_OK) return st;
@@ -989,6 +980,10 @@ extern "C" qp_status qp_linear_fwd_sharded_p2p(const qp_layer* shard, const void
     if (!y_peers[k] || !flag_peers[k]) return fail(QP_ERR_INVALID_ARG, "peer %d pointer is NULL", k);
   if (flags & (QP_Y_ACCUMULATE | QP_FUSE_RHT))
     return fail(QP_ERR_INVALID_ARG, "qp_linear_fwd_sharded_p2p: QP_Y_ACCUMULATE / QP_FUSE_RHT not supported");
+  // round entry barrier: no rank stores round n into a peer's y_full before that peer has entered
+  // round n (its stream-ordered readers of round n-1 are done)
+  if (cudaError_t e = launch_peer_enter(flag_peers, rank, world, static_cast<cudaStream_t>(stream)); e != cudaSuccess)
+    return cuda_fail(e, "peer enter kernel launch");
   // every final value is written once, by its owner, to every rank: the in-order epilogue
   const PeerOut po{world, rank, rank * shard->d_out, world * shard->d_out, y_peers, flag_peers};
   g_peer_out = &po;
@@ -1000,27 +995,71 @@ extern "C" qp_status qp_linear_fwd_sharded_p2p(const qp_layer* shard, const void
   return QP_OK;
 }
 
-extern "C" qp_status qp_ipc_handle(const void* dev_ptr, void* handle64) {
-  if (!dev_ptr || !handle64) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_ipc_handle");
-  cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
-  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
-  std::memcpy(handle64, &h, 64);
+extern "C" qp_status qp_gather_permute(const void* src, void* dst, int world, int batch, int m, int elem_bytes,
+                                       void* stream) {
+  if (!src || !dst) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_gather_permute");
+  if (world < 1 || batch < 1 || m < 1 || (elem_bytes != 2 && elem_bytes != 4))
+    return fail(QP_ERR_INVALID_ARG, "qp_gather_permute: world %d batch %d m %d elem_bytes %d", world, batch, m,
+                elem_bytes);
+  cudaError_t e = launch_gather_permute(src, dst, world, batch, m, elem_bytes, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "gather permute");
   return QP_OK;
 }
 
-extern "C" qp_status qp_ipc_open(const void* handle64, void** dev_ptr) {
-  if (!dev_ptr || !handle64) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_ipc_open");
+namespace {
+// cuMemGetAddressRange through the runtime's driver entry point (no link-time libcuda dependency):
+// base and size of the allocation containing ptr. IPC handles name whole allocations, and PyTorch's
+// caching allocator (or qp_set_allocator) hands out pointers inside larger segments.
+using AddrRangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+cudaError_t alloc_base(const void* ptr, uintptr_t* base) {
+  static AddrRangeFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !f) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    fn = reinterpret_cast<AddrRangeFn>(f);
+  }
+  unsigned long long b = 0;
+  size_t n = 0;
+  if (fn(&b, &n, (unsigned long long)reinterpret_cast<uintptr_t>(ptr)) != 0) return cudaErrorInvalidValue;
+  *base = (uintptr_t)b;
+  return cudaSuccess;
+}
+}  // namespace
+
+extern "C" qp_status qp_ipc_handle(const void* dev_ptr, void* handle72) {
+  if (!dev_ptr || !handle72) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_ipc_handle");
+  uintptr_t base = 0;
+  cudaError_t e = alloc_base(dev_ptr, &base);
+  if (e != cudaSuccess) return cuda_fail(e, "cuMemGetAddressRange");
   cudaIpcMemHandle_t h;
-  std::memcpy(&h, handle64, 64);
-  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  const uint64_t off = (uint64_t)(reinterpret_cast<uintptr_t>(dev_ptr) - base);
+  std::memcpy(handle72, &h, 64);
+  std::memcpy(static_cast<uint8_t*>(handle72) + 64, &off, 8);
+  return QP_OK;
+}
+
+extern "C" qp_status qp_ipc_open(const void* handle72, void** dev_ptr) {
+  if (!dev_ptr || !handle72) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_ipc_open");
+  cudaIpcMemHandle_t h;
+  uint64_t off = 0;
+  std::memcpy(&h, handle72, 64);
+  std::memcpy(&off, static_cast<const uint8_t*>(handle72) + 64, 8);
+  void* base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  *dev_ptr = static_cast<uint8_t*>(base) + off;
   return QP_OK;
 }
 
 extern "C" qp_status qp_ipc_close(void* dev_ptr) {
-  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  uintptr_t base = 0;
+  cudaError_t e = alloc_base(dev_ptr, &base);
+  if (e == cudaSuccess) e = cudaIpcCloseMemHandle(reinterpret_cast<void*>(base));
   if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
   return QP_OK;
 }

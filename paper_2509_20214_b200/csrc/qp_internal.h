@@ -166,6 +166,11 @@ int gemv_smem_bytes(int nwarps);
 cudaError_t launch_rht(const RhtParams& p, bool pdl, cudaStream_t s);
 cudaError_t launch_zero(const RhtParams& p, int grid, bool pdl, cudaStream_t s);   // only the n_zero/zero_* fields
 cudaError_t launch_peer_wait(unsigned* flags_local, int world, cudaStream_t s);
+struct PeerFlags {
+  int world, rank;
+  unsigned* peers[kMaxGroup];   // every rank's flag array [2 * world + 1] (mapped here)
+};
+cudaError_t launch_peer_enter(unsigned* const* flag_peers, int rank, int world, cudaStream_t s);
 cudaError_t launch_gather_permute(const void* src, void* dst, int world, int batch, int m, int elem_bytes,
                                   cudaStream_t s);
 void count_launch();

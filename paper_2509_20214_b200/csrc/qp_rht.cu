@@ -188,16 +188,61 @@ __global__ void qp_gather_permute_kernel(const uint8_t* __restrict__ src, uint8_
 __global__ void qp_peer_wait_kernel(unsigned* flags_local, int world) {
   if (threadIdx.x != 0) return;
   const unsigned want = flags_local[world] + 1u;
+  const unsigned long long t0 = gtimer_ns();
   for (int q = 0; q < world; ++q) {
     unsigned v;
     for (;;) {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags_local + q) : "memory");
       if ((int)(v - want) >= 0) break;
+      if (gtimer_ns() - t0 > kPeerTimeoutNs) __trap();
       __nanosleep(64);
     }
   }
   flags_local[world] = want;
   __threadfence_system();
+}
+
+// Spin-wait guard of the cross-rank waits: a peer that never arrives (a crashed or mismatched rank)
+// traps after ~20 s instead of hanging the GPU; the host sees QP_ERR_CUDA on a later call.
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+// Start of a fused all-gather round on this rank: announce to every peer that this rank has entered
+// round n (so its readers of round n-1's y_full, earlier on its stream, are done): bump
+// flag_peers[k][world + 1 + rank]; then wait until every peer has entered round n too
+// (flags_local[world + 1 + k] >= flags_local[world] + 1, the rounds this rank has consumed + 1).
+// Only then may this rank store round n into the peers' y_full.
+__global__ void qp_peer_enter_kernel(PeerFlags f) {
+  if (threadIdx.x != 0) return;
+  const int world = f.world;
+  for (int k = 0; k < world; ++k) atomicAdd_system(f.peers[k] + world + 1 + f.rank, 1u);
+  __threadfence_system();
+  unsigned* local = f.peers[f.rank];
+  const unsigned want = local[world] + 1u;
+  const unsigned long long t0 = gtimer_ns();
+  for (int k = 0; k < world; ++k) {
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(local + world + 1 + k) : "memory");
+      if ((int)(v - want) >= 0) break;
+      if (gtimer_ns() - t0 > kPeerTimeoutNs) __trap();
+      __nanosleep(64);
+    }
+  }
+}
+
+cudaError_t launch_peer_enter(unsigned* const* flag_peers, int rank, int world, cudaStream_t s) {
+  PeerFlags f{};
+  f.world = world;
+  f.rank = rank;
+  for (int k = 0; k < world; ++k) f.peers[k] = flag_peers[k];
+  qp_peer_enter_kernel<<<1, 32, 0, s>>>(f);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_peer_wait(unsigned* flags_local, int world, cudaStream_t s) {

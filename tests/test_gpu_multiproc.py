@@ -1,0 +1,126 @@
+"""The row-sharded path across processes on ONE GPU (the gpurun box has one B200): 2 and 4 ranks,
+each a process with its own CUDA context on device 0, exchange CUDA-IPC handles through a gloo
+process group and run qp_layer_shard + qp_linear_fwd_sharded_p2p (the fused all-gather epilogue:
+peer stores into every rank's y_full, per-rank completion flags, the round-entry barrier and the
+wait kernel). Every rank's gathered y_full must equal the float64 oracle on the full layer
+(2e-3 normwise), over repeated rounds (eager and CUDA-graph replays) with y_full reused every
+round. Also qp_gather_permute (the [P][B][m] -> [B][P*m] step after ncclAllGather) at P = 2/4/8.
+
+NCCL itself refuses two ranks on one device, so qp_linear_fwd_sharded's ncclAllGather runs only at
+world 1 here (tests/test_gpu_parity.py); the permutation it applies afterwards is tested below.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+SEED = 7
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cases, results):
+    import torch.distributed as dist
+    from oracle import linear
+    from paper_2509_20214_b200 import _lib as L
+    from qp_synth import activations_fp16, channel_scales, random_code_bytes
+    from tests import qp_cases as Q
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for ci, (scheme, x4, d_out, d_in, batch, ydt) in enumerate(cases):
+            cb = L.Codebook(scheme, x4, Q.load_fp16(scheme, x4), L=16)
+            r = L.Rht(SEED, d_in)
+            codes = random_code_bytes(Q.code_bytes(d_out, d_in, scheme, x4), 60 + ci)
+            s = channel_scales(d_out, d_in)
+            full = L.Layer.from_codes(codes, s, d_out, d_in, scheme, x4, cb, r)
+            shard = full.shard(rank, world)
+            m = d_out // world
+            dtype = torch.float32 if ydt == "f32" else torch.float16
+            pg = L.PeerGather(world, rank, m, batch, dtype=dtype)
+            errs = []
+            print(f"[rank {rank}] case {ci} shard ready", flush=True)
+            st = torch.cuda.Stream()
+            for rnd in range(3):
+                # a different input every round: stale data from the previous round would show
+                x = activations_fp16(batch, d_in, seed=100 + rnd)
+                ref = linear.linear_from_codes(codes, d_out, d_in, scheme, x4, Q.oracle_codebook(scheme, x4), s,
+                                               x.astype(np.float64), SEED)
+                xg = torch.from_numpy(x).cuda()
+                with torch.cuda.stream(st):
+                    pg.forward(shard, xg, stream=st)
+                    yh = pg.y.float().cpu().numpy()            # the reader of this round (same stream)
+                errs.append(float(np.max(linear.normwise_error(yh, ref))))
+                print(f"[rank {rank}] case {ci} round {rnd} err {errs[-1]:.2e}", flush=True)
+            # CUDA graph of one round, replayed with the input changing in place
+            x = activations_fp16(batch, d_in, seed=200)
+            xg = torch.from_numpy(x).cuda()
+            with torch.cuda.stream(st):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    pg.forward(shard, xg, stream=st)
+                for rep in range(3):
+                    xn = activations_fp16(batch, d_in, seed=300 + rep)
+                    xg.copy_(torch.from_numpy(xn))
+                    g.replay()
+                    yh = pg.y.float().cpu().numpy()
+                    ref = linear.linear_from_codes(codes, d_out, d_in, scheme, x4, Q.oracle_codebook(scheme, x4), s,
+                                                   xn.astype(np.float64), SEED)
+                    errs.append(float(np.max(linear.normwise_error(yh, ref))))
+            torch.cuda.synchronize()
+            dist.barrier()
+            results[(rank, ci)] = max(errs)
+            pg.close()
+            del pg, shard, full
+            torch.cuda.synchronize()
+            dist.barrier()
+    except Exception as e:                       # report, do not hang the other ranks
+        results[(rank, -1)] = repr(e)
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+CASES = [("tcq", 10, 512, 1024, 1, "f32"), ("vq", 12, 256, 512, 3, "f16"), ("half_tcq", 13, 1024, 1024, 8, "f32")]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_p2p_allgather_across_processes(world):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), CASES, results), nprocs=world, join=True)
+    errs = dict(results)
+    assert all(k[1] >= 0 for k in errs), errs
+    assert len(errs) == world * len(CASES), errs
+    assert max(errs.values()) <= TOL, errs
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("batch", [1, 3, 8])
+def test_gather_permute(world, batch):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_20214_b200 import _lib as L
+    m = 96
+    for dtype in (torch.float32, torch.float16):
+        src = torch.randn(world, batch, m, device="cuda").to(dtype)
+        dst = torch.empty(batch, world * m, dtype=dtype, device="cuda")
+        L.gather_permute(src, dst, world, batch, m)
+        torch.cuda.synchronize()
+        assert torch.equal(dst, src.permute(1, 0, 2).reshape(batch, world * m))

@@ -275,12 +275,17 @@ def test_offline_quantizer_c1_matches_oracle():
     Lb = _need_gpu()
     from qp_synth import gaussian_weights
     cb, ocb = _pair("tcq", 8, L=12)
+    alpha = Q.tcq_alpha("tcq", 8, L=12)                # reading R22 (codebooks/tcq_alpha.json)
+    cb.set_scale(alpha)
     W = gaussian_weights(256, 256, seed=0)
-    lay = Lb.Layer.quantize_offline(W.astype(np.float32), "tcq", 8, cb, Lb.Rht(SEED, 256))
+    try:
+        lay = Lb.Layer.quantize_offline(W.astype(np.float32), "tcq", 8, cb, Lb.Rht(SEED, 256))
+    finally:
+        cb.set_scale(1.0)
     codes_g, s_g = lay.codes(), lay.scales()
-    codes_o, s_o = linear.quantize_offline(W.astype(np.float32).astype(np.float64), "tcq", 8, ocb, SEED)
+    codes_o, s_o = linear.quantize_offline(W.astype(np.float32).astype(np.float64), "tcq", 8, ocb, SEED, alpha=alpha)
     assert np.allclose(s_g, s_o, rtol=1e-6)
-    Wt, _ = linear.gaussianize(W.astype(np.float32).astype(np.float64), SEED)
+    Wt, _ = linear.gaussianize(W.astype(np.float32).astype(np.float64), SEED, alpha)
     Wg = decode.decode_layer(codes_g, 256, 256, "tcq", 8, ocb)
     Wo = decode.decode_layer(codes_o, 256, 256, "tcq", 8, ocb)
     dg, do = np.sum((Wg - Wt) ** 2), np.sum((Wo - Wt) ** 2)
@@ -440,15 +445,21 @@ def test_gpu_trellis_encoder_matches_host_and_oracle(d_out, d_in, scheme, bits_x
     Lb = _need_gpu()
     from qp_synth import gaussian_weights
     cb, ocb = _pair(scheme, bits_x4, L=L)
+    alpha = Q.tcq_alpha(scheme, bits_x4, L=L)           # reading R22
     W = gaussian_weights(d_out, d_in, seed=0).astype(np.float32)
     r = Lb.Rht(SEED, d_in)
-    lay_g = Lb.Layer.quantize_offline(W, scheme, bits_x4, cb, r, gpu=True)
-    lay_h = Lb.Layer.quantize_offline(W, scheme, bits_x4, cb, r)
+    cb.set_scale(alpha)
+    try:
+        lay_g = Lb.Layer.quantize_offline(W, scheme, bits_x4, cb, r, gpu=True)
+        lay_h = Lb.Layer.quantize_offline(W, scheme, bits_x4, cb, r)
+    finally:
+        cb.set_scale(1.0)
     codes_g, codes_h = lay_g.codes(), lay_h.codes()
     assert np.array_equal(codes_g, codes_h)
     assert np.array_equal(lay_g.scales(), lay_h.scales())
-    Wt, _ = linear.gaussianize(W.astype(np.float64), SEED)
-    codes_o, _ = linear.quantize_offline(W.astype(np.float64), scheme, bits_x4, ocb, SEED)
+    Wt, s_o = linear.gaussianize(W.astype(np.float64), SEED, alpha)
+    assert np.allclose(lay_g.scales(), s_o, rtol=1e-6)
+    codes_o, _ = linear.quantize_offline(W.astype(np.float64), scheme, bits_x4, ocb, SEED, alpha=alpha)
     Wg = decode.decode_layer(codes_g, d_out, d_in, scheme, bits_x4, ocb)
     Wo = decode.decode_layer(codes_o, d_out, d_in, scheme, bits_x4, ocb)
     dg, do = np.sum((Wg - Wt) ** 2), np.sum((Wo - Wt) ** 2)
@@ -456,7 +467,7 @@ def test_gpu_trellis_encoder_matches_host_and_oracle(d_out, d_in, scheme, bits_x
 
 
 @pytest.mark.parametrize("scheme,bits_x4,tol", [
-    ("tcq", 8, 0.02),    # P:909 Ours-TCQ-2 (L = 16, T = 256, tlut_bits = 9)
+    ("tcq", 8, 0.02),    # P:909 Ours-TCQ-2 (L = 16, T = 256, tlut_bits = 9, alpha of reading R22)
     ("vq", 8, 0.02),     # P:911 Ours-VQ-2 (our k-means codebook: reading R21)
     ("nuq", 8, 0.005),   # P:910 Ours-NUQ-2
 ])
@@ -468,12 +479,19 @@ def test_table5_distortion_at_scale(scheme, bits_x4, tol):
     Lb = _need_gpu()
     from qp_synth import gaussian_weights
     cb, _ = _pair(scheme, bits_x4, L=16)
+    alpha = Q.tcq_alpha(scheme, bits_x4)               # reading R22 (1 for VQ / NUQ)
     d_out, d_in = 1024, 4096
     W = gaussian_weights(d_out, d_in, seed=0).astype(np.float32)
-    lay = Lb.Layer.quantize_offline(W, scheme, bits_x4, cb, Lb.Rht(SEED, d_in), gpu=True)
+    cb.set_scale(alpha)
+    try:
+        lay = Lb.Layer.quantize_offline(W, scheme, bits_x4, cb, Lb.Rht(SEED, d_in), gpu=True)
+    finally:
+        cb.set_scale(1.0)
     W_hat = _dequant_gpu(lay).astype(np.float64)
-    Wt, _ = linear.gaussianize(W.astype(np.float64), SEED)
-    d = float(np.mean((Wt - W_hat) ** 2))
+    Wt, s1 = linear.gaussianize(W.astype(np.float64), SEED)
+    # reconstruction of the standardized rows: (stored scale / s) * W_hat = alpha * W_hat
+    rec = W_hat * (lay.scales().astype(np.float64) / s1)[:, None]
+    d = float(np.mean((Wt - rec) ** 2))
     from . import golden_values as G
     paper = G.table5(f"{scheme}-2.0")                 # tests/golden/table5_distortion.json
     assert abs(d - paper) / paper < tol, d

@@ -35,6 +35,16 @@ def load_fp16(scheme: str, bits_x4: int) -> np.ndarray:
     return np.fromfile(codebook_path(scheme, bits_x4), dtype="<f2")
 
 
+def tcq_alpha(scheme: str, bits_x4: int, L: int = 16) -> float:
+    """Reconstruction scale of the TCQ codebook at this width (reading R22, codebooks/tcq_alpha.json);
+    1 for NUQ / UNIF / VQ."""
+    if scheme not in ("tcq", "half_tcq"):
+        return 1.0
+    import json
+    d = json.load(open(os.path.join(os.path.dirname(codebook_path("tcq", 8)), "tcq_alpha.json")))
+    return float(d[f"{scheme}/{bits_x4}/L{L}"]["alpha"])
+
+
 def code_bytes(d_out: int, d_in: int, scheme: str, bits_x4: int) -> int:
     return d_out * d_in * bits_x4 // 32
 

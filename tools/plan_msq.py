@@ -42,7 +42,10 @@ def distortion(scheme, x4, cbs, rots, rows=256, d_in=4096):
         rots[d_in].apply(Wg[r0:r0 + 8], 8, Wr[r0:r0 + 8])
     s = torch.from_numpy(lay.scales()).cuda()
     Wt = Wr.float() / s[:, None]
-    return float(((Wt - Wh.float()) ** 2).mean())
+    # the stored scales are s * alpha (reading R22): the error of the unit-RMS rows is alpha^2 times
+    # the error measured against W'/(s alpha)
+    a = cbs[(scheme, x4)].alpha
+    return float(((Wt - Wh.float()) ** 2).mean()) * a * a
 
 
 def group_latency(name, d_out, d_in, scheme, x4, cbs, rots, l2):
@@ -82,7 +85,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "msq.jsonl"))
     a = ap.parse_args()
     qs = P.TARGET if a.quantizers == "target" else P.PALETTE
-    cbs = {(s, x): QL.Codebook(s, x, P.load_fp16(s, x), L=16) for s, x in qs}
+    cbs = {(s, x): QL.Codebook(s, x, P.load_fp16(s, x), L=16, alpha=P.tcq_alpha(s, x)) for s, x in qs}
     rots = {d: QL.Rht(7, d) for d in (H, FF)}
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
