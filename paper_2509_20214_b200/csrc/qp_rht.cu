@@ -182,6 +182,15 @@ __global__ void qp_gather_permute_kernel(const uint8_t* __restrict__ src, uint8_
   }
 }
 
+// Spin-wait guard of the cross-rank waits: a peer that never arrives (a crashed or mismatched rank)
+// traps after ~20 s instead of hanging the GPU; the host sees QP_ERR_CUDA on a later call.
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
 // Fused all-gather completion on this rank: flags_local[q] counts the launches rank q has
 // completed into our y_full; flags_local[world] is how many we have consumed. Waits until every
 // rank is one ahead, then consumes (graph-replay safe: no host-side epoch).
@@ -202,14 +211,6 @@ __global__ void qp_peer_wait_kernel(unsigned* flags_local, int world) {
   __threadfence_system();
 }
 
-// Spin-wait guard of the cross-rank waits: a peer that never arrives (a crashed or mismatched rank)
-// traps after ~20 s instead of hanging the GPU; the host sees QP_ERR_CUDA on a later call.
-__device__ __forceinline__ unsigned long long gtimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
 
 // Start of a fused all-gather round on this rank: announce to every peer that this rank has entered
 // round n (so its readers of round n-1's y_full, earlier on its stream, are done): bump
