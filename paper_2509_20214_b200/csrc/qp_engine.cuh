@@ -203,37 +203,48 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   const uint32_t ring = smem_u32(smem + PL::RING_OFF) + (uint32_t)(warp * NS * PL::STAGE);
   const uint32_t bars = smem_u32(smem + PL::BAR_OFF) + (uint32_t)(warp * NS * 8);
   // Copy the tile d positions after the decode cursor (oi_, rt_, kt_, left_, opk_) into stage st
-  // (lane 0 issues). Warp-uniform address arithmetic, no live fetch cursor: the same row in one
-  // add, a row / layer boundary by a short loop.
-  auto fetch_ahead = [&](int st, uint32_t dep, uint32_t d, int oi_, uint32_t rt_, uint32_t kt_, uint32_t left_,
-                         uint32_t opk_) {
-    if (d < left_ && kt_ + d < (opk_ & 0xffu)) {
-      kt_ += d;
-    } else if (d < left_) {
+  // (lane 0 issues). f_ptr is the address following the previous copy: inside a layer the tiles of
+  // a warp's range are contiguous (row-tile-major, k order), so the next copy starts there and only
+  // its size (c of its k tile) is computed; the first copy and a copy into a later layer compute the
+  // address from scratch.
+  const uint8_t* f_ptr = nullptr;
+  auto fetch_ahead = [&](int st, uint32_t dep, uint32_t d, bool cont, int oi_, uint32_t rt_, uint32_t kt_,
+                         uint32_t left_, uint32_t opk_) {
+    const uint8_t* src;
+    if (cont && d < left_) {                   // same layer as the previous copy: contiguous
       const uint32_t KT_ = opk_ & 0xffu;
       kt_ += d;
-      while (kt_ >= KT_) { kt_ -= KT_; ++rt_; }
-    } else {                                   // in a later layer
-      d -= left_;
-      ++oi_;
-      while (oi_ + 1 < p.n_ops && d >= (uint32_t)(p.op[oi_].RT * p.op[oi_].KT)) {
-        d -= (uint32_t)(p.op[oi_].RT * p.op[oi_].KT);
+      while (kt_ >= KT_) kt_ -= KT_;
+      src = f_ptr;
+    } else {
+      if (d < left_) {
+        const uint32_t KT_ = opk_ & 0xffu;
+        kt_ += d;
+        while (kt_ >= KT_) { kt_ -= KT_; ++rt_; }
+      } else {                                 // in a later layer
+        d -= left_;
         ++oi_;
+        while (oi_ + 1 < p.n_ops && d >= (uint32_t)(p.op[oi_].RT * p.op[oi_].KT)) {
+          d -= (uint32_t)(p.op[oi_].RT * p.op[oi_].KT);
+          ++oi_;
+        }
+        opk_ = pack(oi_);
+        rt_ = d / (opk_ & 0xffu);
+        kt_ = d - rt_ * (opk_ & 0xffu);
       }
-      opk_ = pack(oi_);
-      rt_ = d / (opk_ & 0xffu);
-      kt_ = d - rt_ * (opk_ & 0xffu);
+      const EngOp& o = p.op[oi_];
+      const uint32_t KH_ = (opk_ >> 8) & 0xffu, clo = (opk_ >> 16) & 0xffu, chi = opk_ >> 24;
+      src = o.codes + (long long)rt_ * o.rowtile_bytes +
+            (kt_ < KH_ ? kt_ * 512u * clo : KH_ * 512u * clo + (kt_ - KH_) * 512u * chi);
     }
-    const EngOp& o = p.op[oi_];
-    const uint32_t KH_ = (opk_ >> 8) & 0xffu, clo = (opk_ >> 16) & 0xffu, chi = opk_ >> 24;
-    const uint8_t* src = o.codes + (long long)rt_ * o.rowtile_bytes +
-                         (kt_ < KH_ ? kt_ * 512u * clo : KH_ * 512u * clo + (kt_ - KH_) * 512u * chi);
-    const uint32_t nb = 512u * (kt_ < KH_ ? clo : chi);
+    const uint32_t KH_ = (opk_ >> 8) & 0xffu;
+    const uint32_t nb = 512u * (kt_ < KH_ ? (opk_ >> 16) & 0xffu : opk_ >> 24);
     if (lane == 0) {
       const uint32_t bar = bars + 8u * st;
       mbar_expect_tx(bar, nb);
       bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, src, nb, bar, l2_evict_first_policy());
     }
+    f_ptr = src + nb;
   };
 
   // ---- rotation jobs (the first CTAs): x' of every layer, before this CTA's own tiles ------------
@@ -260,10 +271,10 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     mbar_fence_init();
   }
   __syncwarp();
-  if (a < b) fetch_ahead(0, 0u, 0u, oi, rt, kt, left, opk);
+  if (a < b) fetch_ahead(0, 0u, 0u, false, oi, rt, kt, left, opk);
   QP_TL(2);
   tbl.store(smem);
-  for (int st = 1; st < NS && a + st < b; ++st) fetch_ahead(st, 0u, (uint32_t)st, oi, rt, kt, left, opk);
+  for (int st = 1; st < NS && a + st < b; ++st) fetch_ahead(st, 0u, (uint32_t)st, true, oi, rt, kt, left, opk);
   if (!rotor) asm volatile("griddepcontrol.wait;" ::: "memory");
   QP_TL(3);
   __syncthreads();
@@ -302,12 +313,13 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   for (int i = 0; i < 32; ++i) xb[i] = 0u;
   // this lane's x' row (g) and column group (q) of layer o_
   auto xlane = [&](int o_) -> const __half* { return p.op[o_].xr + (size_t)g * p.op[o_].d_in + 64 * q; };
+  const __half* xl = nullptr;            // this lane's x' row of the current layer
   if (a < b) {
     enter_op(oi);
     QP_TL(4);
     load_scales(oi, rt);
+    xl = xlane(oi);
     if (xrow) {
-      const __half* xl = xlane(oi);
       load_x8_coh(xb, xl + kt * kTileCols);
       load_x8_coh(xb + 8, xl + kt * kTileCols + 16);
     }
@@ -327,7 +339,6 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     const bool row_end = kt + 1 == KT;
     const bool op_end = left == 1u;       // the last tile of this layer
     // first-half activations of the next tile are loaded mid-tile when it is in the same layer
-    const __half* xl = xlane(opaque(oi));
     const __half* x_hi = xrow ? xl + kt * kTileCols + 32 : nullptr;
     const __half* x_next = (xrow && t + 1 < b && !op_end) ? xl + (row_end ? 0u : kt + 1) * kTileCols : nullptr;
     const uint32_t src = ring + (uint32_t)(st * PL::STAGE) + (uint32_t)lane * 16u;
@@ -341,7 +352,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       }
       // the stage is free once every lane's shared loads have returned (see qp_gemv_kernel)
       const uint32_t dep = __reduce_or_sync(0xffffffffu, cur[4 * C - 1] & p.zero);
-      if (t + NS < b) fetch_ahead(st, dep, (uint32_t)NS, opaque(oi), rt, kt, left, opk);
+      if (t + NS < b) fetch_ahead(st, dep, (uint32_t)NS, true, oi, rt, kt, left, opk);
       tile_body<MODE, C, L, TB, REPS, false, false, true>(cur, laneoff, mulk, xb, acc, nullptr, 0, x_hi, x_next, 0u);
     });
     if (++st == NS) { st = 0; par ^= 1u; }
@@ -422,10 +433,10 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
           opk = pack(on);
           left = (uint32_t)p.op[on].RT * p.op[on].KT;
           enter_op(on);
+          xl = xlane(on);
           if (xrow) {
-            const __half* xn = xlane(on);
-            load_x8_coh(xb, xn);
-            load_x8_coh(xb + 8, xn + 16);
+            load_x8_coh(xb, xl);
+            load_x8_coh(xb + 8, xl + 16);
           }
         }
       }
