@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   if (a < b) fetch_ahead(0, 0u, 0u, false, oi, rt, kt, left, opk);
   QP_TL(2);
   tbl.store(smem);
-  for (int st = 1; st < NS && a + st < b; ++st) fetch_ahead(st, 0u, (uint32_t)st, true, oi, rt, kt, left, opk);
+  if (!p.late_stages)
+    for (int st = 1; st < NS && a + st < b; ++st) fetch_ahead(st, 0u, (uint32_t)st, true, oi, rt, kt, left, opk);
   if (!rotor) asm volatile("griddepcontrol.wait;" ::: "memory");
   QP_TL(3);
   __syncthreads();
@@ -317,6 +318,8 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   if (a < b) {
     enter_op(oi);
     QP_TL(4);
+    if (p.late_stages)
+      for (int st = 1; st < NS && a + st < b; ++st) fetch_ahead(st, 0u, (uint32_t)st, true, oi, rt, kt, left, opk);
     load_scales(oi, rt);
     xl = xlane(oi);
     if (xrow) {
@@ -332,32 +335,49 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   int seg_k0 = (int)kt;
   int st = 0;
   uint32_t par = 0;
-  for (uint32_t t = a; t < b; ++t) {
+  // The loop runs over *runs*: consecutive tiles of one row tile at one step width c (a row tile
+  // is one run, or two for half-TCQ), each run a compile-time-c inner loop whose per-tile work is
+  // only the ring wait, the stage's shared loads, the next copy and the decode; row / layer
+  // transitions and the epilogue happen between runs.
+  for (uint32_t t = a; t < b;) {
     const uint32_t KT = opk & 0xffu, KH = (opk >> 8) & 0xffu;
-    mbar_wait(bars + 8u * st, par);
     const int c = kt < KH ? (int)((opk >> 16) & 0xffu) : (int)(opk >> 24);
-    const bool row_end = kt + 1 == KT;
-    const bool op_end = left == 1u;       // the last tile of this layer
-    // first-half activations of the next tile are loaded mid-tile when it is in the same layer
-    const __half* x_hi = xrow ? xl + kt * kTileCols + 32 : nullptr;
-    const __half* x_next = (xrow && t + 1 < b && !op_end) ? xl + (row_end ? 0u : kt + 1) * kTileCols : nullptr;
-    const uint32_t src = ring + (uint32_t)(st * PL::STAGE) + (uint32_t)lane * 16u;
+    const uint32_t kend = kt < KH ? KH : KT;                 // the run ends at k tile kend (exclusive)
+    const uint32_t n = min(kend - kt, b - t);
+    const bool run_row_end = kt + n == KT;
     c_dispatch<CMIN, CMAX>(c, [&](auto CC) {
       constexpr int C = decltype(CC)::value;
-      uint32_t cur[4 * C];
+#pragma unroll 1
+      for (uint32_t i = 0; i < n; ++i) {
+        mbar_wait(bars + 8u * st, par);
+        const uint32_t src = ring + (uint32_t)(st * PL::STAGE) + (uint32_t)lane * 16u;
+        uint32_t cur[4 * C];
 #pragma unroll
-      for (int i = 0; i < C; ++i) {
-        const uint4 v = lds128(src + i * 512);
-        cur[4 * i] = v.x; cur[4 * i + 1] = v.y; cur[4 * i + 2] = v.z; cur[4 * i + 3] = v.w;
+        for (int w = 0; w < C; ++w) {
+          const uint4 v = lds128(src + w * 512);
+          cur[4 * w] = v.x; cur[4 * w + 1] = v.y; cur[4 * w + 2] = v.z; cur[4 * w + 3] = v.w;
+        }
+        // the stage is free once every lane's shared loads have returned (see qp_gemv_kernel)
+        const uint32_t dep = __reduce_or_sync(0xffffffffu, cur[4 * C - 1] & p.zero);
+        const uint32_t tt = t + i;
+        if (tt + NS < b) fetch_ahead(st, dep, (uint32_t)NS, true, oi, rt, kt, left, opk);
+        // activations: second half of this tile now, first half of the next tile mid-tile when the
+        // next tile is in the same layer (next k tile, or k tile 0 of the next row tile)
+        const bool row_end = kt + 1 == KT;
+        const __half* x_hi = xrow ? xl + kt * kTileCols + 32 : nullptr;
+        const __half* x_next =
+            (xrow && tt + 1 < b && left != 1u) ? xl + (row_end ? 0u : kt + 1) * kTileCols : nullptr;
+        tile_body<MODE, C, L, TB, REPS, false, false, true>(cur, laneoff, mulk, xb, acc, nullptr, 0, x_hi, x_next, 0u);
+        if (++st == NS) { st = 0; par ^= 1u; }
+        --left;
+        ++kt;
       }
-      // the stage is free once every lane's shared loads have returned (see qp_gemv_kernel)
-      const uint32_t dep = __reduce_or_sync(0xffffffffu, cur[4 * C - 1] & p.zero);
-      if (t + NS < b) fetch_ahead(st, dep, (uint32_t)NS, true, oi, rt, kt, left, opk);
-      tile_body<MODE, C, L, TB, REPS, false, false, true>(cur, laneoff, mulk, xb, acc, nullptr, 0, x_hi, x_next, 0u);
     });
-    if (++st == NS) { st = 0; par ^= 1u; }
-
-    if (row_end || t == b - 1) {
+    t += n;
+    --kt;                                  // kt = the run's last k tile (the epilogue's view)
+    const bool row_end = run_row_end;
+    const bool op_end = row_end && left == 0u;
+    if (row_end || t == b) {
       // ---- end of this warp's segment of row tile rt ----
       const int oe = opaque(oi);
       const int d_out = p.op[oe].d_out;
@@ -420,15 +440,14 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
         for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
       seg_k0 = 0;
     }
-    // ---- advance to the next tile ----
-    --left;
+    // ---- advance to the next run ----
     if (row_end) {
       kt = 0;
       ++rt;
       if (op_end) {
         ++oi;
         rt = 0;
-        if (t + 1 < b) {
+        if (t < b) {
           const int on = opaque(oi);
           opk = pack(on);
           left = (uint32_t)p.op[on].RT * p.op[on].KT;
@@ -440,7 +459,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
           }
         }
       }
-      if (t + 1 < b) load_scales(opaque(oi), rt);
+      if (t < b) load_scales(opaque(oi), rt);
     } else {
       ++kt;
     }

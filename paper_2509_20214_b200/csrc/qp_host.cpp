@@ -1120,6 +1120,14 @@ bool same_table(const qp_codebook* a, const qp_codebook* b) {
   return a == b || (a->mode == b->mode && a->L == b->L && a->tb == b->tb && a->reps == b->reps &&
                     a->table_words == b->table_words && a->host == b->host);
 }
+int eng_late_stages() {   // QP_ENG_LATE=1: fill ring stages 1.. only once x' is ready (experiment)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QP_ENG_LATE");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
 double eng_job_tiles() {   // QP_ENG_JOB_TILES: tiles of GEMV work one rotation job displaces
   static double v = -1;
   if (v < 0) {
@@ -1285,6 +1293,7 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
     }
     p.total_jobs = jobs;
     p.rot_scratch_bytes = scratch;
+    p.late_stages = eng_late_stages();
     const int grid = (int)std::min<long long>(std::min(num_sms(), kMaxEngCtas), tiles);
     // CTA ranges over the flat tile order; the CTAs that run rotation jobs take job_tiles fewer
     // tiles per job

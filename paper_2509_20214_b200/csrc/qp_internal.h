@@ -137,6 +137,7 @@ struct EngParams {
   int total_jobs;
   int ns;                      // ring stages per warp (set by the launcher)
   int rot_scratch_bytes;       // shared memory the rotation jobs need (b_max * 4)
+  int late_stages;             // 1: ring stages 1.. are first filled after the layer's x' is ready
   uint32_t zero;               // always 0 (an operand the compiler cannot fold)
   const uint32_t* table;       // compact decode table shared by every layer
   unsigned* gen;               // [1]: CTAs out this launch (the last one resets the ready counters)
