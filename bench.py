@@ -180,6 +180,57 @@ def oracle_sample(layers, budget_rows=512, which=None):
     return total_bytes, dt
 
 
+def cpu_info():
+    """CPU model, logical CPUs and the BLAS / OpenMP thread pools (threadpoolctl) of this process."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    pools = []
+    try:
+        from threadpoolctl import threadpool_info
+        pools = [{"api": i.get("user_api"), "lib": i.get("internal_api"), "threads": i.get("num_threads")}
+                 for i in threadpool_info()]
+    except Exception:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "thread_pools": pools}
+
+
+# On-chip ceilings of the fused dequant-GEMV (SURVEY 8(d)), per weight pair: issue slots of the
+# decode + MMA (from the engine's SASS: TCQ SHF + 2 IMAD + LOP3 + LDS + HMMA/4 + code loads ~ 5.3;
+# VQ / NUQ SHF + LOP3 + LDS + HMMA/4 ~ 3.3) at 4 warp-instructions / clk / SM, and one shared-memory
+# LUT wavefront per 32 pairs (1 wavefront / clk / SM).
+ISSUE_PER_PAIR = {"tcq": 5.3, "half_tcq": 5.3, "vq": 3.3, "nuq": 3.3, "unif": 3.3}
+
+
+def ceilings(layers, batch, peak_gbs, sm_mhz, n_sm=148):
+    """Fractions of the HBM roofline the step could reach if bound by issue slots, by shared-memory
+    LUT wavefronts, or by the slower of the two per layer (time-weighted over the step)."""
+    f = (sm_mhz or 1965.0) * 1e6
+    t_hbm = t_issue = t_smem = t_all = 0.0
+    nbytes = 0
+    for L in layers:
+        g, r = layer_bytes(L["d_out"], L["d_in"], L["bits_x4"], L["tb"], batch)
+        pairs = L["d_out"] * L["d_in"] / 2
+        th = (g + r) / (peak_gbs * 1e9)
+        ti = pairs * ISSUE_PER_PAIR[L["scheme"]] / (128.0 * n_sm * f)
+        ts = pairs / (32.0 * n_sm * f)
+        t_hbm += th
+        t_issue += max(th, ti)
+        t_smem += max(th, ts)
+        t_all += max(th, ti, ts)
+        nbytes += g + r
+    return {"issue_frac": round(t_hbm / t_issue, 4), "smem_frac": round(t_hbm / t_smem, 4),
+            "frac": round(t_hbm / t_all, 4), "sm_mhz": sm_mhz,
+            "model": "per layer max(HBM bytes / peak, pairs x issue-slots-per-pair / (4 warp-instr/clk x 32 x "
+                     "148 SMs), pairs / (32/clk x 148 SMs)); issue slots per pair from the engine SASS "
+                     "(TCQ 5.3, VQ/NUQ 3.3)"}
+
+
 def cpu_cores():
     try:
         from threadpoolctl import threadpool_info
@@ -457,19 +508,29 @@ def main():
     #      the launching stream ---------------------------------------------------------------------
     eng = None
     eng_traffic, eng_traffic_src = engine_traffic(batch)
-    if use_engine:
+
+    def time_engine(b_):
+        """us per engine launch at batch b_ (its own activations / outputs, both replicas)."""
+        xs_b = [[torch.from_numpy(activations_fp16(b_, L["d_in"])).to(dev) for L in layers] for _ in range(REPLICAS)]
+        ys_b = [[torch.empty(b_, L["d_out"], dtype=torch.float32, device=dev) for L in layers] for _ in range(REPLICAS)]
         n_rep = 8
+
+        def launch(k):
+            multis[k % REPLICAS].forward(xs_b[k % REPLICAS], b_, ys_b[k % REPLICAS], flags=extra_flags, stream=stream)
         with torch.cuda.stream(stream):
             if eager:
                 def ge_replay():
                     for k in range(n_rep):
-                        step_fn(k % REPLICAS, stream)
+                        launch(k)
                 ge = type("G", (), {"replay": staticmethod(ge_replay)})
             else:
+                for k in range(REPLICAS):
+                    launch(k)
+                stream.synchronize()
                 ge = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(ge, stream=stream):
                     for k in range(n_rep):
-                        step_fn(k % REPLICAS, stream)
+                        launch(k)
             for _ in range(3):
                 ge.replay()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -479,8 +540,23 @@ def main():
                 ge.replay()
             b.record(stream)
             b.synchronize()
-        eng_us = a.elapsed_time(b) * 1e3 / (reps * n_rep)
+        return a.elapsed_time(b) * 1e3 / (reps * n_rep)
+
+    batch_lines = {}
+    if use_engine:
+        eng_us = time_engine(batch)
         eng = {"achieved": step_bytes / (eng_us * 1e-6) / 1e9, "us": eng_us}
+        # the metric spans batch 1-8: the same step at the other batch sizes (engine launch alone)
+        for b_ in (1, 2, 4, 8):
+            if b_ == batch:
+                continue
+            us_b = time_engine(b_)
+            bytes_b = sum(sum(layer_bytes(L["d_out"], L["d_in"], L["bits_x4"], L["tb"], b_)) for L in layers)
+            ach = bytes_b / (us_b * 1e-6) / 1e9
+            batch_lines[f"b{b_}"] = {"us_per_step": round(us_b, 3), "us_per_layer": round(us_b / n_layers, 3),
+                                     "achieved_gbs": round(ach, 1), "frac": None, "traffic": None}
+            tr, _ = engine_traffic(b_)
+            batch_lines[f"b{b_}"]["traffic"] = round(tr) if tr else None
 
     # ---- end to end through the public API with host buffers (N=1 only) ------------------
     # Every step: one H2D copy of the step's 9 activation vectors from pinned host memory, the 9
@@ -586,10 +662,14 @@ def main():
         nb, dt = oracle_sample(layers, budget_rows=512)
         cpu = {"value": round(nb / dt / 1e9, 6), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
                "sample": "first 512 rows of each of the 9 C2 layers: float64 decode + RHT + matvec (batch 1)",
-               "seconds": round(dt, 2)}
+               "seconds": round(dt, 2), **cpu_info()}
 
     if rank == 0:
         ck = clk.summary()
+        peak_b, _ = measured_peaks()
+        for k, v in batch_lines.items():
+            v["frac"] = round(v["achieved_gbs"] / peak_b, 4)
+            v["ceilings"] = ceilings(layers, int(k[1:]), peak_b, ck.get("sm_mhz"))
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
@@ -613,6 +693,8 @@ def main():
                                     "launch), CUDA graph of back-to-back launches alternating 2 replicas of 163 MB of "
                                     "codes (> L2), events on the launching stream",
                           "peak_kind": peak_kind, "avg_launch_us": round(eng["us"], 3),
+                          "ceilings": ceilings(layers, batch, peak, ck.get("sm_mhz")),
+                          "batches": batch_lines,
                           "per_layer_path": {"achieved": round(gemv_achieved, 1), "frac": round(gemv_achieved / peak, 4),
                                              "avg_launch_us": round(gemv_avg_ms * 1e3, 3),
                                              "kernel": "qp_gemv_kernel alone per layer (pre-rotated x)"}}
