@@ -353,7 +353,7 @@ def main():
     torch.cuda.synchronize()
 
     extra_flags = int(os.environ.get("QP_BENCH_FLAGS", "0"))     # experiments only (e.g. 4 = QP_DETERMINISTIC)
-    use_engine = args.path == "engine" and world == 1
+    use_engine = args.path == "engine"
     multis = []
     if use_engine:
         for rep in range(REPLICAS):
@@ -369,7 +369,11 @@ def main():
     def step_fn(rep, stream):
         """One step: the 9 layers of replica `rep` (rotation + fused dequant-GEMV each)."""
         group = insts[rep * n_layers:(rep + 1) * n_layers]
-        if use_engine:
+        if use_engine and world > 1:
+            # this rank's shards through the engine, then one grouped NCCL all-gather of all 9 outputs
+            multis[rep].forward_sharded([i["x"] for i in group], batch, [i["y"] for i in group], comm,
+                                        flags=extra_flags, stream=stream)
+        elif use_engine:
             multis[rep].forward([i["x"] for i in group], batch, [i["y"] for i in group], flags=extra_flags,
                                 stream=stream)
         else:
@@ -512,7 +516,7 @@ def main():
     def time_engine(b_):
         """us per engine launch at batch b_ (its own activations / outputs, both replicas)."""
         xs_b = [[torch.from_numpy(activations_fp16(b_, L["d_in"])).to(dev) for L in layers] for _ in range(REPLICAS)]
-        ys_b = [[torch.empty(b_, L["d_out"], dtype=torch.float32, device=dev) for L in layers] for _ in range(REPLICAS)]
+        ys_b = [[torch.empty(b_, L["m"], dtype=torch.float32, device=dev) for L in layers] for _ in range(REPLICAS)]
         n_rep = 8
 
         def launch(k):
@@ -544,8 +548,11 @@ def main():
 
     batch_lines = {}
     if use_engine:
+        # (N > 1: the engine alone over this rank's shards, i.e. per-rank bytes / time, no all-gather)
         eng_us = time_engine(batch)
-        eng = {"achieved": step_bytes / (eng_us * 1e-6) / 1e9, "us": eng_us}
+        rank_bytes = gemv_bytes / world + rht_bytes / world
+        eng = {"achieved": rank_bytes / (eng_us * 1e-6) / 1e9, "us": eng_us, "bytes": rank_bytes}
+    if use_engine and world == 1:
         # the metric spans batch 1-8: the same step at the other batch sizes (engine launch alone)
         for b_ in (1, 2, 4, 8):
             if b_ == batch:
@@ -677,7 +684,8 @@ def main():
             "config": {"workload": "C2: Llama-3.1-8B (4096x4096, 14336x4096, 4096x14336) x TCQ-2.5 / half-TCQ-3.25 / "
                                    "TCQ-4.0 (L=16), rotation + fused dequant-GEMV per layer (qp_linear_fwd on raw x)",
                        "batch": batch, "layers_per_step": n_layers, "us_per_layer": round(ms * 1e3 / n_layers, 3),
-                       "parallelism": f"row-shard x{world} + NCCL all-gather" if world > 1 else "single GPU",
+                       "parallelism": (f"row-shard x{world}: engine over each rank's shards + one grouped NCCL "
+                                       f"all-gather per step" if world > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (2 replicas, 326 MB per 2 steps, L2 126 MB)",
                        "graph": "CUDA graph per step, PDL between consecutive kernels",
                        "kernels_per_layer": round(launches_per_step / n_layers, 3),
@@ -688,7 +696,7 @@ def main():
             "roofline": ({"bound": "hbm", "achieved": round(eng["achieved"], 1), "peak": peak, "unit": "GB/s",
                           "frac": round(eng["achieved"] / peak, 4),
                           "traffic": round(eng_traffic) if eng_traffic else None, "traffic_source": eng_traffic_src,
-                          "algorithmic_bytes_per_launch": int(step_bytes),
+                          "algorithmic_bytes_per_launch": int(eng["bytes"]),
                           "kernel": "qp_engine_kernel (persistent: the 9 layers' rotations + fused dequant-GEMVs in one "
                                     "launch), CUDA graph of back-to-back launches alternating 2 replicas of 163 MB of "
                                     "codes (> L2), events on the launching stream",

@@ -180,6 +180,14 @@ qp_status qp_dequantize(const qp_layer* l, void* W_hat_fp16, void* stream);
 qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_multi** out);
 qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype xt, int batch, void* const* ys, qp_dtype yt,
                        unsigned flags, void* stream);
+/* Row-sharded qp_multi_fwd (north star: large layers row-sharded over the node, all-gather of y):
+ * the qp_multi's layers are this rank's shards (qp_layer_shard with the communicator's world size);
+ * the engine computes every shard's rows, then ONE grouped ncclAllGather (ncclGroupStart / End)
+ * assembles ys_full[i] [batch][d_out_i * world] (dtype yt) on every rank, ranks' rows in rank order.
+ * Errors: as qp_multi_fwd, QP_ERR_CONFIG_MISMATCH (a layer is not a shard of this world size),
+ * QP_ERR_NCCL (incl. an asynchronous NCCL fault of an earlier call); QP_Y_ACCUMULATE is rejected. */
+qp_status qp_multi_fwd_sharded(qp_multi* m, const void* const* xs, qp_dtype xt, int batch, void* const* ys_full,
+                               qp_dtype yt, void* comm, unsigned flags, void* stream);
 /* n_layers; launch groups per qp_multi_fwd (n_launches: one engine launch each, or the per-layer
  * qp_linear_fwd path for a layer without an engine variant); how many are engine launches. */
 qp_status qp_multi_info(const qp_multi* m, int* n_layers, int* n_launches, int* n_engine_launches);

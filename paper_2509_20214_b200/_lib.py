@@ -37,6 +37,7 @@ EXPORTS = [
     "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range", "qp_optimal_bits", "qp_plan_msq",
     "qp_linear_fwd_sharded_p2p", "qp_ipc_handle", "qp_ipc_open", "qp_ipc_close",
     "qp_codebook_set_scale", "qp_gather_permute", "qp_multi_create", "qp_multi_fwd", "qp_multi_info", "qp_multi_free",
+    "qp_multi_fwd_sharded",
 ]
 
 
@@ -64,6 +65,7 @@ def lib() -> C.CDLL:
             "qp_multi_create": [C.POINTER(vp), i, C.POINTER(vp)],
             "qp_multi_fwd": [vp, C.POINTER(vp), i, i, C.POINTER(vp), i, C.c_uint, vp],
             "qp_multi_info": [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i)],
+            "qp_multi_fwd_sharded": [vp, C.POINTER(vp), i, i, C.POINTER(vp), i, vp, C.c_uint, vp],
             "qp_multi_free": [vp],
             "qp_rht_create": [u64, i, i, C.POINTER(vp)],
             "qp_rht_free": [vp],
@@ -297,6 +299,13 @@ class Multi:
         ya = (C.c_void_p * len(ys))(*[_ptr(y) for y in ys])
         check(lib().qp_multi_fwd(self.h, xa, _dtype_code(xs[0]), batch, ya, _dtype_code(ys[0]), flags,
                                  _stream(stream)))
+
+    def forward_sharded(self, xs: list, batch: int, ys_full: list, comm, flags: int = 0, stream=None) -> None:
+        """qp_multi_fwd_sharded: the layers are shards; ys_full[i] receives all ranks' rows."""
+        xa = (C.c_void_p * len(xs))(*[_ptr(x) for x in xs])
+        ya = (C.c_void_p * len(ys_full))(*[_ptr(y) for y in ys_full])
+        check(lib().qp_multi_fwd_sharded(self.h, xa, _dtype_code(xs[0]), batch, ya, _dtype_code(ys_full[0]), comm.h,
+                                         flags, _stream(stream)))
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:

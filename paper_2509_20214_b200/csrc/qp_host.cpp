@@ -964,6 +964,9 @@ qp_status qp_linear_fwd_sharded(const qp_layer* shard, const void* x, qp_dtype x
     cudaError_t e = launch_gather_permute(gathered, y_full, world, batch, m, eb, s);
     if (e != cudaSuccess) return cuda_fail(e, "gather permute");
   }
+  ncclResult_t ae = ncclSuccess;   // asynchronous NCCL faults of earlier calls surface here
+  if (ncclCommGetAsyncError(c, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+    return fail(QP_ERR_NCCL, "asynchronous NCCL error: %s", ncclGetErrorString(ae));
   return QP_OK;
 }
 
@@ -1312,5 +1315,58 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
     if (e != cudaSuccess) return cuda_fail(e, "engine launch");
     count_launch();
   }
+  return QP_OK;
+}
+
+// Row-sharded multi-layer forward: the engine over this rank's shards (one persistent launch per
+// table family) into each shard's local scratch, then ONE grouped NCCL all-gather of every layer's
+// rows (ncclGroupStart / End: a single collective launch over NVLink / NVSwitch), then the
+// [P][B][m] -> [B][P m] permutation for batch > 1.
+extern "C" qp_status qp_multi_fwd_sharded(qp_multi* m, const void* const* xs, qp_dtype xt, int batch,
+                                          void* const* ys_full, qp_dtype yt, void* comm, unsigned flags,
+                                          void* stream) {
+  if (!m || !xs || !ys_full || !comm) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_multi_fwd_sharded");
+  if (flags & QP_Y_ACCUMULATE)
+    return fail(QP_ERR_INVALID_ARG, "qp_multi_fwd_sharded: QP_Y_ACCUMULATE is not supported (the all-gather "
+                "overwrites y_full)");
+  ncclComm_t c = static_cast<ncclComm_t>(comm);
+  int world = 0;
+  if (ncclCommCount(c, &world) != ncclSuccess || world < 1) return fail(QP_ERR_NCCL, "ncclCommCount failed");
+  const int n = (int)m->layers.size();
+  const int eb = yt == QP_F32 ? 4 : 2;
+  std::vector<void*> local(n);
+  for (int i = 0; i < n; ++i) {
+    const qp_layer* l = m->layers[i];
+    if (!ys_full[i]) return fail(QP_ERR_INVALID_ARG, "ys_full[%d] is NULL", i);
+    if (l->gather_bytes < (size_t)(world + 1) * batch * l->d_out * eb)
+      return fail(QP_ERR_CONFIG_MISMATCH, "qp_multi_fwd_sharded: layer %d is not a shard of a %d-rank split "
+                  "(qp_layer_shard)", i, world);
+    local[i] = l->d_gather;
+  }
+  qp_status st = qp_multi_fwd(m, xs, xt, batch, local.data(), yt, flags, stream);
+  if (st != QP_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ncclResult_t r = ncclGroupStart();
+  for (int i = 0; i < n && r == ncclSuccess; ++i) {
+    const qp_layer* l = m->layers[i];
+    uint8_t* gathered = static_cast<uint8_t*>(l->d_gather) + (size_t)batch * l->d_out * eb;
+    r = ncclAllGather(local[i], batch == 1 ? ys_full[i] : gathered, (size_t)batch * l->d_out,
+                      yt == QP_F32 ? ncclFloat32 : ncclFloat16, c, s);
+  }
+  ncclResult_t r2 = ncclGroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess)
+    return fail(QP_ERR_NCCL, "grouped ncclAllGather: %s", ncclGetErrorString(r != ncclSuccess ? r : r2));
+  if (batch > 1) {
+    for (int i = 0; i < n; ++i) {
+      const qp_layer* l = m->layers[i];
+      uint8_t* gathered = static_cast<uint8_t*>(l->d_gather) + (size_t)batch * l->d_out * eb;
+      cudaError_t e = launch_gather_permute(gathered, ys_full[i], world, batch, l->d_out, eb, s);
+      if (e != cudaSuccess) return cuda_fail(e, "gather permute");
+    }
+  }
+  // asynchronous NCCL faults of earlier collectives surface here (header contract)
+  ncclResult_t ae = ncclSuccess;
+  if (ncclCommGetAsyncError(c, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+    return fail(QP_ERR_NCCL, "asynchronous NCCL error: %s", ncclGetErrorString(ae));
   return QP_OK;
 }

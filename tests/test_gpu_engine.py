@@ -236,3 +236,27 @@ def test_c2_full_size_engine(c2_reference, batch, y_dtype):
     for it, y, r in zip(items, ys, refs):
         err = np.max(linear.normwise_error(y.float().cpu().numpy(), r[:batch]))
         assert err <= TOL, (it[0].d_out, it[0].d_in, it[5], err)
+
+
+@pytest.mark.parametrize("batch", [1, 4])
+def test_engine_sharded_nccl_world1(batch):
+    """qp_multi_fwd_sharded at world size 1 (one GPU per gpurun box): the engine over the shards,
+    one grouped ncclAllGather, the permutation for batch > 1 -- against the oracle."""
+    Lb = _lib()
+    items = _make(TB9_MIX[:4], first_id=140)
+    comm = Lb.NcclComm(Lb.NcclComm.unique_id(), 1, 0)
+    try:
+        shards = [it[0].shard(0, 1) for it in items]
+        m = Lb.Multi(shards)
+        xs_np = [activations_fp16(batch, it[0].d_in, seed=61 + i) for i, it in enumerate(items)]
+        xs = [torch.from_numpy(x).cuda() for x in xs_np]
+        ys = [torch.empty(batch, it[0].d_out, dtype=torch.float32, device="cuda") for it in items]
+        for _ in range(2):
+            m.forward_sharded(xs, batch, ys, comm)
+        torch.cuda.synchronize()
+        for it, x, y in zip(items, xs_np, ys):
+            assert np.max(linear.normwise_error(y.cpu().numpy(), _ref(it, x))) <= TOL
+        with pytest.raises(Lb.QPError):                       # full layers are not shards
+            Lb.Multi([it[0] for it in items]).forward_sharded(xs, batch, ys, comm)
+    finally:
+        comm.close()
