@@ -39,6 +39,14 @@ __device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+// one elected lane of the (converged) warp: the compiler keeps the guarded operands in uniform
+// registers (a plain lane == 0 test makes it move them through a per-lane waterfall loop)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -168,7 +176,10 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   const int NS = p.ns;
   uint8_t* smem = qp_smem;
   if (threadIdx.x == 0 && smem_u32(qp_smem) != kDynSmemBase) __trap();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warp index through a lane-0 broadcast: provably warp-uniform to the compiler, so the ring /
+  // range / fetch arithmetic derived from it lives in uniform registers (no per-copy waterfall loop
+  // to feed the bulk copy's uniform operands)
+  const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int g = lane >> 2, q = lane & 3;
   QP_TL(0);
 
@@ -239,7 +250,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     }
     const uint32_t KH_ = (opk_ >> 8) & 0xffu;
     const uint32_t nb = 512u * (kt_ < KH_ ? (opk_ >> 16) & 0xffu : opk_ >> 24);
-    if (lane == 0) {
+    if (elect_one()) {
       const uint32_t bar = bars + 8u * st;
       mbar_expect_tx(bar, nb);
       bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, src, nb, bar, l2_evict_first_policy());

@@ -15,6 +15,7 @@ struct Register {
     EngineVariant<DEC_LUT2, 0, 0, 32, 6, 6>::reg();              // VQ 3.0, NUQ / UNIF 3
     EngineVariant<DEC_LUT2, 0, 0, 32, 7, 7>::reg();              // VQ 3.5
     EngineVariant<DEC_LUT2, 0, 0, 32, 8, 8>::reg();              // VQ 4.0, NUQ / UNIF 4
+    EngineVariant<DEC_LUT2, 0, 0, 32, 9, 9>::reg();              // VQ 4.5
   }
 } register_instance;
 }  // namespace

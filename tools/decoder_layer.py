@@ -12,6 +12,8 @@ q/o 3.94, k/v 4.94, MLP 3.04 bits. Palette assignment:
   * o (3.94): NUQ-4;   up / gate (3.04): TCQ-3.0 (fused group);   down (3.04): VQ-3.0.
 One step = the 4 ops of a decoder layer, each = rotation of its input + fused dequant-GEMV
 (qp_fused_linear / qp_linear_fwd), in one CUDA graph; R replicas of the layer (> 2x L2) cycle.
+--engine: the 7 matrices through one qp_multi_fwd call instead (the persistent engine: one launch
+per decode-table family = 4 launches, q / k / v and gate / up as separate layers of one launch).
 The ops use independent synthetic inputs (no attention / activation function between them: the
 path measured is the quantized linear layers).
 """
@@ -53,6 +55,7 @@ def main():
     ap.add_argument("--batches", default="1,8")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "c5.jsonl"))
+    ap.add_argument("--engine", action="store_true")
     a = ap.parse_args()
     bits, qkv_bits = allocation()
     shapes = {m: (o, i) for m, o, i in MATS}
@@ -76,7 +79,10 @@ def main():
                 codes = random_code_bytes(P.code_bytes(d_out, d_in, scheme, x4), 1000 + 10 * r + j)
                 lays.append(QL.Layer.from_codes(codes, channel_scales(d_out, d_in), d_out, d_in, scheme, x4,
                                                 cbs[key], rots[d_in]))
-            ops.append((members, QL.Group(lays) if len(lays) > 1 else lays[0], lays, d_in))
+            ops.append((members, QL.Group(lays) if len(lays) > 1 and not a.engine else lays[0], lays, d_in))
+        if a.engine:
+            ops = [("multi", QL.Multi([l for _, _, ls, _ in ops for l in ls]),
+                    [m for ms, _, _, _ in ops for m in ms], [d for ms, _, _, d in ops for _ in ms])]
         reps.append(ops)
     peak, _ = P.hbm_peak()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
@@ -93,6 +99,10 @@ def main():
         st = torch.cuda.Stream()
 
         def step(ops):
+            if a.engine:
+                _, multi, mats, d_ins = ops[0]
+                multi.forward([xs[d] for d in d_ins], batch, [ys[m] for m in mats], stream=st)
+                return
             for members, op, lays, d_in in ops:
                 if isinstance(op, QL.Group):
                     op.forward(xs[d_in], batch, [ys[m] for m in members], stream=st)
@@ -120,6 +130,7 @@ def main():
             e1.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / (5 * K)
         line = {"config": "C5: Llama-3.1-8B decoder layer, mixed schemes, fused QKV / up-gate", "batch": batch,
+                "path": "engine (qp_multi_fwd)" if a.engine else "per op (qp_fused_linear / qp_linear_fwd)",
                 "us_per_decoder_layer": round(us, 3), "alg_bytes": alg, "gbs": round(alg / us / 1e3, 1),
                 "frac_of_hbm_peak": round(alg / us / 1e3 / peak, 4), "peak_gbs": peak, "kernels_per_layer": launches,
                 "replicas": R, "allocation_bits": bits, "qkv_group_bits": qkv_bits,

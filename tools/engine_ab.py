@@ -31,6 +31,16 @@ SETS = {
 }
 
 
+def palette_sets():
+    """C3 through the engine: every target quantizer (2-4.5 bits) over the three C2 shapes, one
+    engine launch per set (the 3 layers of one quantizer share its decode table)."""
+    from tests import qp_cases as Q
+    out = {}
+    for s, x4 in Q.TARGET:
+        out[f"c3:{s}:{x4}"] = [(o, i, s, x4) for o, i in SHAPES]
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sets", default="c2,c2_tcq25,c2_tcq40,c2_half325,big_tcq25,sq_tcq25")
@@ -38,7 +48,12 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--prerotated", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph (for ncu)")
+    ap.add_argument("--palette", action="store_true", help="C3: every target quantizer over the C2 shapes")
+    ap.add_argument("--batches", default="")
     args = ap.parse_args()
+    if args.palette:
+        SETS.update(palette_sets())
+        args.sets = ",".join(k for k in SETS if k.startswith("c3:"))
     import torch
     from paper_2509_20214_b200 import _lib as QL
     from qp_synth import activations_fp16, channel_scales, random_code_bytes
@@ -46,8 +61,8 @@ def main():
     torch.cuda.set_device(0)
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     cbs, rots = {}, {}
-    B = args.batch
-    for name in args.sets.split(","):
+    batches = [int(b) for b in args.batches.split(",")] if args.batches else [args.batch]
+    for name, B in [(n, b) for n in args.sets.split(",") for b in batches]:
         specs = SETS[name]
         nbytes = sum(Q.code_bytes(o, i, s, x) for o, i, s, x in specs)
         n_rep = max(2, -(-2 * l2 // nbytes) + 1)
@@ -55,7 +70,7 @@ def main():
         alg = 0
         for o, i, s, x in specs:
             b = x / 4
-            tb = 9 if (s != "half_tcq" and b <= 4) or (s == "half_tcq" and b + 0.25 <= 4) else 10
+            tb = Q.tlut_bits(s, x) if s in ("tcq", "half_tcq") else 0
             lut = 4 << tb if s in ("tcq", "half_tcq") else (4 << int(2 * b) if s == "vq" else 2 << int(b))
             alg += Q.code_bytes(o, i, s, x) + 4 * o + lut + 2 * B * i + 4 * B * o + (0 if args.prerotated else 4 * B * i)
         for r in range(n_rep):
@@ -94,8 +109,11 @@ def main():
             b.record(st)
             b.synchronize()
         us = a.elapsed_time(b) * 1e3 / (args.iters * n_rep)
+        from tools import palette as Pal
+        peak, _ = Pal.hbm_peak()
         print(json.dumps({"set": name, "batch": B, "layers": len(specs), "us_per_launch": round(us, 2),
                           "us_per_layer": round(us / len(specs), 3), "gbs": round(alg / (us * 1e-6) / 1e9, 1),
+                          "frac": round(alg / (us * 1e-6) / 1e9 / peak, 4), "engine_launches": multis[0].n_engine_launches,
                           "launches_per_call": multis[0].n_launches, "replicas": n_rep,
                           "prerotated": args.prerotated}), flush=True)
         del multis, xs, ys

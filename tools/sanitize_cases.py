@@ -4,7 +4,8 @@
 
 Covers: rotation kernel, fused GEMV (atomic fp32, deterministic fp32, fp16 y, pre-rotated x,
 y accumulate), x' staged in shared memory (QP_XS path via the fused rotation flag), row-pair units
-(batch 8, VQ), fused groups, dequantize, and the GPU trellis encoder."""
+(batch 8, VQ), fused groups, dequantize, the persistent multi-layer engine (qp_multi_fwd) and the
+GPU trellis encoder."""
 import os
 import sys
 
@@ -56,6 +57,18 @@ def main():
     g = QL.Group(ms)
     x = torch.from_numpy(activations_fp16(2, 512)).cuda()
     g.forward(x, 2, [torch.empty(2, d, device="cuda") for d in (64, 32, 32)])
+    # persistent multi-layer engine: tb = 9 family (rotation jobs with 1 and 7 Hadamard blocks, split
+    # row tiles through the self-cleaning workspace, fp32 / fp16 / accumulate), a VQ group, a fallback
+    specs = [("tcq", 10, 96, 1024), ("half_tcq", 13, 64, 1024), ("tcq", 16, 32, 3584), ("vq", 12, 64, 512),
+             ("unif", 32, 32, 256)]
+    eng = [layer(s_, x_, o_, i_, seed=50 + k) for k, (s_, x_, o_, i_) in enumerate(specs)]
+    m = QL.Multi([e[0] for e in eng])
+    for batch in (1, 3, 8):
+        xs = [torch.from_numpy(activations_fp16(batch, i_)).cuda() for (_, _, _, i_) in specs]
+        ys = [torch.empty(batch, o_, device="cuda") for (_, _, o_, _) in specs]
+        m.forward(xs, batch, ys)
+        m.forward(xs, batch, ys, flags=QL.QP_Y_ACCUMULATE)
+        m.forward(xs, batch, [y.half() for y in ys])
     # GPU trellis encoder
     W = gaussian_weights(32, 256, seed=0).astype(np.float32)
     QL.Layer.quantize_offline(W, "tcq", 10, QL.Codebook("tcq", 10, P.load_fp16("tcq", 10), L=16), QL.Rht(7, 256),
