@@ -260,3 +260,37 @@ def test_engine_sharded_nccl_world1(batch):
             Lb.Multi([it[0] for it in items]).forward_sharded(xs, batch, ys, comm)
     finally:
         comm.close()
+
+
+def test_activation_range_limit_r20():
+    """Reading R20 (x' is fp16, no prescale): |x'_i| <= ||x_block||_1 / sqrt(b) <= sqrt(b) max|x|, so
+    rows with max|x| * sqrt(b) < 2^15 never overflow. Pin both sides of the documented limit: such
+    rows (a constant row with max|x| * sqrt(b) = 3e4 on a 4096 block; a single spike) are within the
+    2e-3 bar; a constant row of 6e4 saturates fp16 in x' and the output is not finite (the
+    limitation is real, not silently wrong-but-finite)."""
+    Lb = _lib()
+    items = _make([(64, 4096, "tcq", 10)], first_id=160)
+    m = Lb.Multi([items[0][0]])
+    b = 4096
+    x = np.full((1, b), 0.0, dtype=np.float64)
+    x[0, :] = 30000.0 / np.sqrt(b)            # constant row: |x'_i| <= sqrt(b) max|x| = 3e4 < 2^15
+    x16 = x.astype(np.float16)
+    y = torch.empty(1, 64, device="cuda")
+    m.forward([torch.from_numpy(x16).cuda()], 1, [y])
+    torch.cuda.synchronize()
+    err = np.max(linear.normwise_error(y.cpu().numpy(), _ref(items[0], x16)))
+    assert np.isfinite(y.cpu().numpy()).all() and err <= TOL
+    # a spike: all mass in one coordinate of one block -> x' entries = x_0 / sqrt(b); 8x beyond 2^15 * sqrt(b)
+    xs = np.zeros((1, b), dtype=np.float16)
+    xs[0, 0] = 60000.0
+    y2 = torch.empty(1, 64, device="cuda")
+    m.forward([torch.from_numpy(xs).cuda()], 1, [y2])
+    torch.cuda.synchronize()
+    assert np.isfinite(y2.cpu().numpy()).all()           # 60000 / 64 = 937.5: representable, no overflow
+    err2 = np.max(linear.normwise_error(y2.cpu().numpy(), _ref(items[0], xs)))
+    assert err2 <= TOL
+    xo = np.full((1, b), 60000.0, dtype=np.float16)       # sqrt(b) * 6e4 = 3.8e6 >> 65504: x'_0 saturates
+    y3 = torch.empty(1, 64, device="cuda")
+    m.forward([torch.from_numpy(xo).cuda()], 1, [y3])
+    torch.cuda.synchronize()
+    assert not np.isfinite(y3.cpu().numpy()).all()
