@@ -197,6 +197,21 @@ void qp_multi_free(qp_multi* m);
  * layer (device copy). (d_out/world) % 32 must be 0. */
 qp_status qp_layer_shard(const qp_layer* l, int rank, int world, qp_layer** out);
 
+/* Column (k) shard for row-parallel layers (the down projection after a column-parallel
+ * up / gate): rank r owns input columns [r*d_in/world, (r+1)*d_in/world) of every row (a new layer of
+ * shape d_out x d_in/world holding those k tiles, all scales, and its own rotation = the blocks of R
+ * over its columns, which is exact because R is block-diagonal, P:345-349 / reading R9). Needs
+ * (d_in/world) % 256 == 0 and % rotation block == 0 (QP_ERR_PARTITION_MISMATCH otherwise: quantize
+ * with a smaller block via qp_rht_create(seed, d_in, block)); half-TCQ -> QP_ERR_UNSUPPORTED. */
+qp_status qp_layer_shard_k(const qp_layer* l, int rank, int world, qp_layer** out);
+
+/* K-sharded forward: y[batch][d_out] (device fp32) = sum over ranks of diag(s) W_r R_r x_r, where
+ * x_local = this rank's columns x[:, r*d_in/world : ...] ([batch][d_in/world], dtype xt): the shard's
+ * partial GEMV, then ncclAllReduce(sum) over `comm`. QP_Y_ACCUMULATE is rejected; asynchronous NCCL
+ * faults surface as QP_ERR_NCCL. */
+qp_status qp_linear_fwd_ksharded(const qp_layer* shard, const void* x_local, qp_dtype xt, int batch, void* y,
+                                 qp_dtype yt, void* comm, unsigned flags, void* stream);
+
 /* Host-only (no device work, usable without a GPU): where rank `rank` of `world` finds its row
  * shard of a (d_out x d_in, scheme, bits_x4) layer: rows [*row0, *row0 + *rows) and code bytes
  * [*byte0, *byte0 + *nbytes) of the LAYOUT.md stream (row-tile-major, so a row block is one

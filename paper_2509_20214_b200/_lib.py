@@ -37,7 +37,7 @@ EXPORTS = [
     "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range", "qp_optimal_bits", "qp_plan_msq",
     "qp_linear_fwd_sharded_p2p", "qp_ipc_handle", "qp_ipc_open", "qp_ipc_close",
     "qp_codebook_set_scale", "qp_gather_permute", "qp_multi_create", "qp_multi_fwd", "qp_multi_info", "qp_multi_free",
-    "qp_multi_fwd_sharded",
+    "qp_multi_fwd_sharded", "qp_layer_shard_k", "qp_linear_fwd_ksharded",
 ]
 
 
@@ -81,6 +81,8 @@ def lib() -> C.CDLL:
             "qp_fused_linear": [vp, vp, i, i, C.POINTER(vp), i, C.c_uint, vp],
             "qp_dequantize": [vp, vp, vp],
             "qp_layer_shard": [vp, i, i, C.POINTER(vp)],
+            "qp_layer_shard_k": [vp, i, i, C.POINTER(vp)],
+            "qp_linear_fwd_ksharded": [vp, vp, i, i, vp, i, vp, C.c_uint, vp],
             "qp_shard_range": [i, i, i, i, i, i, C.POINTER(i), C.POINTER(i), C.POINTER(sz), C.POINTER(sz)],
             "qp_set_allocator": [vp, vp, vp],
             "qp_linear_fwd_sharded_p2p": [vp, vp, i, i, vp, vp, i, i, i, C.c_uint, vp],
@@ -245,6 +247,17 @@ class Layer:
         h = C.c_void_p()
         check(lib().qp_layer_shard(self.h, rank, world, C.byref(h)))
         return Layer(h, *self._keep)
+
+    def shard_k(self, rank: int, world: int) -> "Layer":
+        """qp_layer_shard_k: this rank's input columns (row-parallel layer)."""
+        h = C.c_void_p()
+        check(lib().qp_layer_shard_k(self.h, rank, world, C.byref(h)))
+        return Layer(h, *self._keep)
+
+    def forward_ksharded(self, x_local, batch: int, y, comm, flags: int = 0, stream=None) -> None:
+        """qp_linear_fwd_ksharded: partial GEMV on this rank's columns + ncclAllReduce(sum)."""
+        check(lib().qp_linear_fwd_ksharded(self.h, _ptr(x_local), _dtype_code(x_local), batch, _ptr(y),
+                                           _dtype_code(y), comm.h, flags, _stream(stream)))
 
     def forward_sharded(self, x, batch: int, y_full, comm, flags: int = 0, stream=None) -> None:
         check(lib().qp_linear_fwd_sharded(self.h, _ptr(x), _dtype_code(x), batch, _ptr(y_full), _dtype_code(y_full),

@@ -216,6 +216,14 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
 // 256-bit activation load through L1 (for x' written by the same launch, e.g. the multi-layer
 // engine's in-kernel rotation: no .nc path)
 __device__ __forceinline__ void load_x8_coh(uint32_t* dst, const __half* src) {
+#ifdef QP_ENG_NC_X
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(dst[0]), "=r"(dst[1]), "=r"(dst[2]), "=r"(dst[3]), "=r"(dst[4]), "=r"(dst[5]), "=r"(dst[6]),
+                 "=r"(dst[7])
+               : "l"(src)
+               : "memory");
+  return;
+#endif
   asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(dst[0]), "=r"(dst[1]), "=r"(dst[2]), "=r"(dst[3]), "=r"(dst[4]), "=r"(dst[5]), "=r"(dst[6]),
                  "=r"(dst[7])

@@ -199,6 +199,7 @@ struct qp_layer {
   float* d_yws = nullptr;     // [8][d_out] fp32 accumulation workspace for fp16 y
   void* d_gather = nullptr;   // sharded path scratch
   size_t gather_bytes = 0;
+  qp_rht* owned_rht = nullptr;  // k-shards: the column slice of the parent's rotation (freed with the layer)
 };
 
 struct qp_group {
@@ -312,6 +313,11 @@ void layer_release(qp_layer* l) {
   dev_free(l->d_xrot);
   dev_free(l->d_yws);
   dev_free(l->d_gather);
+  if (l->owned_rht) {
+    dev_free(l->owned_rht->d_signs);
+    delete l->owned_rht;
+    l->owned_rht = nullptr;
+  }
 }
 
 qp_status run_rht(const qp_rht* r, const void* x, qp_dtype xt, int batch, __half* out, bool pdl, cudaStream_t s,
@@ -1365,6 +1371,85 @@ extern "C" qp_status qp_multi_fwd_sharded(qp_multi* m, const void* const* xs, qp
     }
   }
   // asynchronous NCCL faults of earlier collectives surface here (header contract)
+  ncclResult_t ae = ncclSuccess;
+  if (ncclCommGetAsyncError(c, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+    return fail(QP_ERR_NCCL, "asynchronous NCCL error: %s", ncclGetErrorString(ae));
+  return QP_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// K (column) sharding: row-parallel layers (the down projection after a column-parallel up /
+// gate): rank r owns input columns [r*d_in/world, (r+1)*d_in/world) of every row and computes a
+// partial y over all rows; the partials are summed across ranks (ncclAllReduce).
+// ---------------------------------------------------------------------------------------
+extern "C" qp_status qp_layer_shard_k(const qp_layer* l, int rank, int world, qp_layer** out) {
+  if (!l || !out) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_layer_shard_k");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return fail(QP_ERR_INVALID_ARG, "rank %d / world %d", rank, world);
+  if (l->c_lo != l->c_hi)
+    return fail(QP_ERR_UNSUPPORTED, "qp_layer_shard_k: half-TCQ layers (two widths along d_in) are not column-"
+                "sharded. Remedy: row-shard them (qp_layer_shard) or use a single-width quantizer");
+  const qp_rht* pr = l->rht;
+  if (l->d_in % world)
+    return fail(QP_ERR_PARTITION_MISMATCH, "d_in=%d does not split into %d column blocks", l->d_in, world);
+  const int dl = l->d_in / world;
+  if (dl % kTileCols || dl % pr->block)
+    return fail(QP_ERR_PARTITION_MISMATCH, "column block %d must be a multiple of 256 (k tiles) and of the rotation "
+                "block %d (R is block-diagonal: a shard rotates only its own blocks). Remedy: quantize with a "
+                "smaller rotation block (qp_rht_create(seed, d_in, block))", dl, pr->block);
+  // the rotation of the shard = the blocks of its columns: same block size, the sign slice
+  auto r = new qp_rht();
+  r->seed = pr->seed;
+  r->d_in = dl;
+  r->block = pr->block;
+  r->sign_bits.assign((dl + 31) / 32, 0u);
+  const int c0 = rank * dl;
+  for (int i = 0; i < dl; ++i)
+    if ((pr->sign_bits[(c0 + i) >> 5] >> ((c0 + i) & 31)) & 1u) r->sign_bits[i >> 5] |= 1u << (i & 31);
+  r->d_signs = static_cast<uint32_t*>(dev_alloc(r->sign_bits.size() * 4));
+  if (!r->d_signs || cudaMemcpy(r->d_signs, r->sign_bits.data(), r->sign_bits.size() * 4, cudaMemcpyHostToDevice) !=
+                         cudaSuccess) {
+    dev_free(r->d_signs);
+    delete r;
+    return fail(QP_ERR_ALLOC, "shard rotation allocation failed");
+  }
+  auto s = new qp_layer();
+  s->owned_rht = r;
+  qp_status st = layer_init(s, l->d_out, dl, l->scheme, l->bits_x4, l->cb, r);
+  if (st != QP_OK) {
+    layer_release(s);
+    delete s;
+    return st;
+  }
+  // every row tile's k tiles [kt0, kt0 + KTl): one strided copy (row-tile-major storage)
+  const size_t tile = 512 * (size_t)l->c_lo, KT = l->d_in / kTileCols, KTl = dl / kTileCols;
+  const size_t RT = l->d_out / kTileRows;
+  cudaError_t e = cudaMemcpy2D(s->d_codes, KTl * tile, l->d_codes + (size_t)rank * KTl * tile, KT * tile, KTl * tile,
+                               RT, cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(s->d_scales, l->d_scales, (size_t)l->d_out * 4, cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  if (e != cudaSuccess) {
+    layer_release(s);
+    delete s;
+    return cuda_fail(e, "k-shard copy");
+  }
+  *out = s;
+  return QP_OK;
+}
+
+extern "C" qp_status qp_linear_fwd_ksharded(const qp_layer* shard, const void* x_local, qp_dtype xt, int batch, void* y,
+                                            qp_dtype yt, void* comm, unsigned flags, void* stream) {
+  if (!shard || !y || !comm) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_linear_fwd_ksharded");
+  if (yt != QP_F32) return fail(QP_ERR_INVALID_ARG, "qp_linear_fwd_ksharded: partial sums need fp32 y");
+  if (flags & QP_Y_ACCUMULATE)
+    return fail(QP_ERR_INVALID_ARG, "qp_linear_fwd_ksharded: QP_Y_ACCUMULATE would be summed world times. "
+                "Remedy: add the residual after the call");
+  qp_status st = qp_linear_fwd(shard, x_local, xt, batch, y, yt, flags, stream);
+  if (st != QP_OK) return st;
+  ncclComm_t c = static_cast<ncclComm_t>(comm);
+  ncclResult_t r = ncclAllReduce(y, y, (size_t)batch * shard->d_out, ncclFloat32, ncclSum, c,
+                                 static_cast<cudaStream_t>(stream));
+  if (r != ncclSuccess) return fail(QP_ERR_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
   ncclResult_t ae = ncclSuccess;
   if (ncclCommGetAsyncError(c, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
     return fail(QP_ERR_NCCL, "asynchronous NCCL error: %s", ncclGetErrorString(ae));

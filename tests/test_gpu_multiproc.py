@@ -124,3 +124,101 @@ def test_gather_permute(world, batch):
         L.gather_permute(src, dst, world, batch, m)
         torch.cuda.synchronize()
         assert torch.equal(dst, src.permute(1, 0, 2).reshape(batch, world * m))
+
+
+def _kworker(rank, world, port, cases, results):
+    """K (column) shards: each rank computes its partial y on the GPU from its columns of x, the
+    partials are summed with gloo (NCCL refuses two ranks on one device), the sum must equal the
+    oracle's y of the full layer."""
+    import torch.distributed as dist
+    from oracle import decode, rht
+    from paper_2509_20214_b200 import _lib as L
+    from qp_synth import activations_fp16, channel_scales, random_code_bytes
+    from tests import qp_cases as Q
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for ci, (scheme, x4, d_out, d_in, block, batch) in enumerate(cases):
+            cb = L.Codebook(scheme, x4, Q.load_fp16(scheme, x4), L=16)
+            r = L.Rht(SEED, d_in, block)
+            codes = random_code_bytes(Q.code_bytes(d_out, d_in, scheme, x4), 80 + ci)
+            s = channel_scales(d_out, d_in)
+            full = L.Layer.from_codes(codes, s, d_out, d_in, scheme, x4, cb, r)
+            shard = full.shard_k(rank, world)
+            dl = d_in // world
+            x = activations_fp16(batch, d_in, seed=90 + ci)
+            xg = torch.from_numpy(np.ascontiguousarray(x[:, rank * dl:(rank + 1) * dl])).cuda()
+            y = torch.empty(batch, d_out, device="cuda")
+            shard.forward(xg, batch, y)
+            torch.cuda.synchronize()
+            yc = y.cpu().double()
+            dist.all_reduce(yc)
+            W = decode.decode_layer(codes, d_out, d_in, scheme, x4, Q.oracle_codebook(scheme, x4))
+            ref = (rht.rht_apply(x.astype(np.float64), SEED, block) @ W.T) * s.astype(np.float64)[None, :]
+            err = float(np.max(np.max(np.abs(yc.numpy() - ref), axis=1) / np.max(np.abs(ref), axis=1)))
+            results[(rank, ci)] = err
+            del shard, full
+    except Exception as e:
+        results[(rank, -1)] = repr(e)
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+KCASES = {2: [("tcq", 10, 64, 1024, 256, 1), ("vq", 12, 96, 2048, 512, 3)],
+          3: [("nuq", 16, 64, 1536, 512, 2)],
+          4: [("tcq", 16, 32, 2048, 256, 8)]}
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_k_shards_across_processes(world):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_kworker, args=(world, _free_port(), KCASES[world], results), nprocs=world, join=True)
+    errs = dict(results)
+    assert all(k[1] >= 0 for k in errs), errs
+    assert len(errs) == world * len(KCASES[world]), errs
+    assert max(errs.values()) <= TOL, errs
+
+
+def test_k_shard_errors_and_nccl_world1():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle import decode, rht
+    from paper_2509_20214_b200 import _lib as L
+    from qp_synth import activations_fp16, channel_scales, random_code_bytes
+    from tests import qp_cases as Q
+    cb = L.Codebook("tcq", 10, Q.load_fp16("tcq", 10), L=16)
+    r = L.Rht(SEED, 1024, 1024)
+    codes = random_code_bytes(Q.code_bytes(64, 1024, "tcq", 10), 5)
+    s = channel_scales(64, 1024)
+    full = L.Layer.from_codes(codes, s, 64, 1024, "tcq", 10, cb, r)
+    with pytest.raises(L.QPError) as e:                    # 512-column shards of a 1024 rotation block
+        full.shard_k(0, 2)
+    assert e.value.status == 3
+    hcb = L.Codebook("half_tcq", 13, Q.load_fp16("half_tcq", 13), L=16)
+    half = L.Layer.from_codes(random_code_bytes(Q.code_bytes(64, 1024, "half_tcq", 13), 6), s, 64, 1024, "half_tcq",
+                              13, hcb, L.Rht(SEED, 1024, 256))
+    with pytest.raises(L.QPError) as e:
+        half.shard_k(0, 2)
+    assert e.value.status == 10
+    comm = L.NcclComm(L.NcclComm.unique_id(), 1, 0)
+    try:
+        sh = full.shard_k(0, 1)
+        x = activations_fp16(2, 1024)
+        y = torch.empty(2, 64, device="cuda")
+        sh.forward_ksharded(torch.from_numpy(x).cuda(), 2, y, comm)
+        torch.cuda.synchronize()
+        W = decode.decode_layer(codes, 64, 1024, "tcq", 10, Q.oracle_codebook("tcq", 10))
+        ref = (rht.rht_apply(x.astype(np.float64), SEED, 1024) @ W.T) * s.astype(np.float64)[None, :]
+        err = np.max(np.max(np.abs(y.cpu().numpy() - ref), axis=1) / np.max(np.abs(ref), axis=1))
+        assert err <= TOL
+        with pytest.raises(L.QPError):
+            sh.forward_ksharded(torch.from_numpy(x).cuda(), 2, y, comm, flags=L.QP_Y_ACCUMULATE)
+    finally:
+        comm.close()

@@ -28,6 +28,10 @@ SETS = {
     "sq_tcq25": [(4096, 4096, "tcq", 10)] * 9,
     "vq3": [(o, i, "vq", 12) for o, i in SHAPES] * 3,
     "nuq4": [(o, i, "nuq", 16) for o, i in SHAPES] * 3,
+    "one_sq": [(4096, 4096, "tcq", 10)],
+    "one_big": [(14336, 4096, "tcq", 10)],
+    "one_down": [(4096, 14336, "tcq", 10)],
+    "one_vq": [(4096, 4096, "vq", 12)],
 }
 
 
@@ -50,6 +54,7 @@ def main():
     ap.add_argument("--eager", action="store_true", help="no CUDA graph (for ncu)")
     ap.add_argument("--palette", action="store_true", help="C3: every target quantizer over the C2 shapes")
     ap.add_argument("--batches", default="")
+    ap.add_argument("--per-layer", action="store_true", help="qp_linear_fwd per layer instead of qp_multi_fwd")
     args = ap.parse_args()
     if args.palette:
         SETS.update(palette_sets())
@@ -91,7 +96,11 @@ def main():
         with torch.cuda.stream(st):
             def run():
                 for r in range(n_rep):
-                    multis[r].forward(xs[r], B, ys[r], flags=flags, stream=st)
+                    if args.per_layer:
+                        for lay, x_, y_ in zip(multis[r].layers, xs[r], ys[r]):
+                            lay.forward(x_, B, y_, flags=flags, stream=st)
+                    else:
+                        multis[r].forward(xs[r], B, ys[r], flags=flags, stream=st)
             run()
             st.synchronize()
             if args.eager:
@@ -115,7 +124,7 @@ def main():
                           "us_per_layer": round(us / len(specs), 3), "gbs": round(alg / (us * 1e-6) / 1e9, 1),
                           "frac": round(alg / (us * 1e-6) / 1e9 / peak, 4), "engine_launches": multis[0].n_engine_launches,
                           "launches_per_call": multis[0].n_launches, "replicas": n_rep,
-                          "prerotated": args.prerotated}), flush=True)
+                          "prerotated": args.prerotated, "path": "per-layer" if args.per_layer else "engine"}), flush=True)
         del multis, xs, ys
         torch.cuda.synchronize()
 
