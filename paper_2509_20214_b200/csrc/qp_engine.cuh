@@ -168,7 +168,10 @@ __device__ unsigned long long g_eng_tl[kMaxEngCtas][8];
 #define QP_TL(k) do { } while (0)
 #endif
 
-template <int MODE, int L, int TB, int REPS, int CMIN, int CMAX>
+// RP: row tiles per work unit. RP = 2 (batch >= 4): a unit is the two row tiles of a row pair at one
+// k tile, decoded back to back with the same activation fragments -- half the x' loads, which are
+// the batch-8 bottleneck (MIO: 4 KB of x' per 32x256 tile at batch 8).
+template <int MODE, int L, int TB, int REPS, int CMIN, int CMAX, int RP>
 __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 32, 1)
     qp_engine_kernel(const __grid_constant__ EngParams p) {
   using PL = EPlan<MODE, L, TB, REPS, CMIN, CMAX>;
@@ -186,8 +189,8 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   TableBuild<REPS, NWARP * 32, PL::ENTRIES> tbl;
   tbl.load(p.table);
 
-  // ---- this warp's tiles: [a, b) of the flat order (host-computed CTA ranges, split evenly over
-  //      the CTA's warps) ------------------------------------------------------------------------
+  // ---- this warp's units: [a, b) of the flat order (host-computed CTA ranges, split evenly over
+  //      the CTA's warps). A unit is RP row tiles (a row pair for RP = 2) at one k tile ----------
   const uint32_t T0 = p.cta_begin[blockIdx.x], T1 = p.cta_begin[blockIdx.x + 1];
   const uint32_t nC = T1 - T0;
   const uint32_t a = T0 + nC * warp / NWARP, b = T0 + nC * (warp + 1) / NWARP;
@@ -196,7 +199,9 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     const EngOp& o = p.op[o_];
     return (uint32_t)o.KT | ((uint32_t)o.KH << 8) | ((uint32_t)o.c_lo << 16) | ((uint32_t)o.c_hi << 24);
   };
-  // decode cursor of tile a: layer oi, row tile rt, k tile kt, geometry opk, tiles left in the layer
+  auto units_of = [&](int o_) -> uint32_t { return (uint32_t)(p.op[o_].RT / RP) * (uint32_t)p.op[o_].KT; };
+  // decode cursor of unit a: layer oi, row group rt (row tiles RP*rt ..), k tile kt, geometry opk,
+  // units left in the layer
   int oi = 0;
   while (oi + 1 < p.n_ops && a >= p.op[oi + 1].tile0) ++oi;
   uint32_t rt, kt, opk = 0, left = 0;
@@ -206,23 +211,22 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     kt = loc - rt * KT_;
     if (a < b) {
       opk = pack(oi);
-      left = (uint32_t)p.op[oi].RT * KT_ - loc;
+      left = units_of(oi) - loc;
     }
   }
 
-  // ---- the code ring -------------------------------------------------------------------------
+  // ---- the code ring (one tile per stage; the tile sequence is unit-major, h = 0..RP-1 inside) --
   const uint32_t ring = smem_u32(smem + PL::RING_OFF) + (uint32_t)(warp * NS * PL::STAGE);
   const uint32_t bars = smem_u32(smem + PL::BAR_OFF) + (uint32_t)(warp * NS * 8);
-  // Copy the tile d positions after the decode cursor (oi_, rt_, kt_, left_, opk_) into stage st
-  // (lane 0 issues). f_ptr is the address following the previous copy: inside a layer the tiles of
-  // a warp's range are contiguous (row-tile-major, k order), so the next copy starts there and only
-  // its size (c of its k tile) is computed; the first copy and a copy into a later layer compute the
-  // address from scratch.
+  // Copy tile h_ of the unit d units after the decode cursor (oi_, rt_, kt_, left_, opk_) into stage
+  // st (an elected lane issues). RP = 1: f_ptr is the address following the previous copy (inside a
+  // layer a warp's tiles are contiguous, row-tile-major), so the next copy starts there; the first
+  // copy, a copy into a later layer and every RP = 2 copy compute the address.
   const uint8_t* f_ptr = nullptr;
-  auto fetch_ahead = [&](int st, uint32_t dep, uint32_t d, bool cont, int oi_, uint32_t rt_, uint32_t kt_,
+  auto fetch_ahead = [&](int st, uint32_t dep, uint32_t d, uint32_t h_, bool cont, int oi_, uint32_t rt_, uint32_t kt_,
                          uint32_t left_, uint32_t opk_) {
     const uint8_t* src;
-    if (cont && d < left_) {                   // same layer as the previous copy: contiguous
+    if (RP == 1 && cont && d < left_) {        // same layer as the previous copy: contiguous
       const uint32_t KT_ = opk_ & 0xffu;
       kt_ += d;
       while (kt_ >= KT_) kt_ -= KT_;
@@ -235,8 +239,8 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       } else {                                 // in a later layer
         d -= left_;
         ++oi_;
-        while (oi_ + 1 < p.n_ops && d >= (uint32_t)(p.op[oi_].RT * p.op[oi_].KT)) {
-          d -= (uint32_t)(p.op[oi_].RT * p.op[oi_].KT);
+        while (oi_ + 1 < p.n_ops && d >= units_of(oi_)) {
+          d -= units_of(oi_);
           ++oi_;
         }
         opk_ = pack(oi_);
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       }
       const EngOp& o = p.op[oi_];
       const uint32_t KH_ = (opk_ >> 8) & 0xffu, clo = (opk_ >> 16) & 0xffu, chi = opk_ >> 24;
-      src = o.codes + (long long)rt_ * o.rowtile_bytes +
+      src = o.codes + (long long)(RP * rt_ + h_) * o.rowtile_bytes +
             (kt_ < KH_ ? kt_ * 512u * clo : KH_ * 512u * clo + (kt_ - KH_) * 512u * chi);
     }
     const uint32_t KH_ = (opk_ >> 8) & 0xffu;
@@ -257,6 +261,8 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     }
     f_ptr = src + nb;
   };
+  // the tile sequence position pos (relative to unit a's first tile) -> (units ahead, h)
+  const uint32_t ntiles = (b - a) * RP;
 
   // ---- rotation jobs (the first CTAs): x' of every layer, before this CTA's own tiles ------------
   const bool rotor = (int)blockIdx.x < p.total_jobs;
@@ -282,18 +288,23 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     mbar_fence_init();
   }
   __syncwarp();
-  if (a < b) fetch_ahead(0, 0u, 0u, false, oi, rt, kt, left, opk);
+  if (a < b) fetch_ahead(0, 0u, 0u, 0u, false, oi, rt, kt, left, opk);
   QP_TL(2);
   tbl.store(smem);
   if (!p.late_stages)
-    for (int st = 1; st < NS && a + st < b; ++st) fetch_ahead(st, 0u, (uint32_t)st, true, oi, rt, kt, left, opk);
+    for (int st = 1; st < NS && (uint32_t)st < ntiles; ++st)
+      fetch_ahead(st, 0u, (uint32_t)st / RP, (uint32_t)st % RP, true, oi, rt, kt, left, opk);
   if (!rotor) asm volatile("griddepcontrol.wait;" ::: "memory");
   QP_TL(3);
   __syncthreads();
 
   const uint32_t laneoff = (uint32_t)(lane % REPS) * 4u;
   const uint32_t mulk = (1u << (Dec<MODE, CMIN, L, TB, REPS>::KSH > 0 ? Dec<MODE, CMIN, L, TB, REPS>::KSH : 0)) + p.zero;
+#ifdef QP_ENG_EXP_XROW1
+  const bool xrow = g < 1;   // experiment: activation loads of batch row 0 only (wrong results for batch > 1)
+#else
   const bool xrow = g < p.batch;
+#endif
   // Register economy: the main loop keeps only a packed copy of the current layer's geometry and
   // the tiles left in it; every other per-layer field is read from the parameter bank where it is
   // needed, through an index the compiler cannot hoist (shfl of the layer index), so no per-layer
@@ -314,11 +325,14 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       (void)ld_acquire_u32(o.ready);
     }
   };
-  float sc[4];
+  float sc[RP][4];
   auto load_scales = [&](int o_, uint32_t rt_) {
-    const float* s = p.op[o_].scales + rt_ * kTileRows + g;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) sc[i] = __ldg(s + 8 * i);
+    for (int h = 0; h < RP; ++h) {
+      const float* s = p.op[o_].scales + (RP * rt_ + h) * kTileRows + g;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sc[h][i] = __ldg(s + 8 * i);
+    }
   };
   uint32_t xb[32];
 #pragma unroll
@@ -330,7 +344,8 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     enter_op(oi);
     QP_TL(4);
     if (p.late_stages)
-      for (int st = 1; st < NS && a + st < b; ++st) fetch_ahead(st, 0u, (uint32_t)st, true, oi, rt, kt, left, opk);
+      for (int st = 1; st < NS && (uint32_t)st < ntiles; ++st)
+        fetch_ahead(st, 0u, (uint32_t)st / RP, (uint32_t)st % RP, true, oi, rt, kt, left, opk);
     load_scales(oi, rt);
     xl = xlane(oi);
     if (xrow) {
@@ -338,15 +353,17 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       load_x8_coh(xb + 8, xl + kt * kTileCols + 16);
     }
   }
-  float acc[2][4];
+  float acc[RP][2][4];
 #pragma unroll
-  for (int m = 0; m < 2; ++m)
+  for (int h = 0; h < RP; ++h)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[h][m][r] = 0.f;
   int seg_k0 = (int)kt;
   int st = 0;
   uint32_t par = 0;
-  // The loop runs over *runs*: consecutive tiles of one row tile at one step width c (a row tile
+  // The loop runs over *runs*: consecutive units of one row group at one step width c (a row group
   // is one run, or two for half-TCQ), each run a compile-time-c inner loop whose per-tile work is
   // only the ring wait, the stage's shared loads, the next copy and the decode; row / layer
   // transitions and the epilogue happen between runs.
@@ -360,26 +377,32 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       constexpr int C = decltype(CC)::value;
 #pragma unroll 1
       for (uint32_t i = 0; i < n; ++i) {
-        mbar_wait(bars + 8u * st, par);
-        const uint32_t src = ring + (uint32_t)(st * PL::STAGE) + (uint32_t)lane * 16u;
-        uint32_t cur[4 * C];
-#pragma unroll
-        for (int w = 0; w < C; ++w) {
-          const uint4 v = lds128(src + w * 512);
-          cur[4 * w] = v.x; cur[4 * w + 1] = v.y; cur[4 * w + 2] = v.z; cur[4 * w + 3] = v.w;
-        }
-        // the stage is free once every lane's shared loads have returned (see qp_gemv_kernel)
-        const uint32_t dep = __reduce_or_sync(0xffffffffu, cur[4 * C - 1] & p.zero);
         const uint32_t tt = t + i;
-        if (tt + NS < b) fetch_ahead(st, dep, (uint32_t)NS, true, oi, rt, kt, left, opk);
-        // activations: second half of this tile now, first half of the next tile mid-tile when the
-        // next tile is in the same layer (next k tile, or k tile 0 of the next row tile)
         const bool row_end = kt + 1 == KT;
-        const __half* x_hi = xrow ? xl + kt * kTileCols + 32 : nullptr;
-        const __half* x_next =
+        // activations: the second half of this k tile at the unit's first tile; the first half of
+        // the next unit's k tile mid-way through its last tile, when that unit is in the same layer
+        const __half* x_nx =
             (xrow && tt + 1 < b && left != 1u) ? xl + (row_end ? 0u : kt + 1) * kTileCols : nullptr;
-        tile_body<MODE, C, L, TB, REPS, false, false, true>(cur, laneoff, mulk, xb, acc, nullptr, 0, x_hi, x_next, 0u);
-        if (++st == NS) { st = 0; par ^= 1u; }
+#pragma unroll
+        for (int h = 0; h < RP; ++h) {
+          mbar_wait(bars + 8u * st, par);
+          const uint32_t src = ring + (uint32_t)(st * PL::STAGE) + (uint32_t)lane * 16u;
+          uint32_t cur[4 * C];
+#pragma unroll
+          for (int w = 0; w < C; ++w) {
+            const uint4 v = lds128(src + w * 512);
+            cur[4 * w] = v.x; cur[4 * w + 1] = v.y; cur[4 * w + 2] = v.z; cur[4 * w + 3] = v.w;
+          }
+          // the stage is free once every lane's shared loads have returned (see qp_gemv_kernel)
+          const uint32_t dep = __reduce_or_sync(0xffffffffu, cur[4 * C - 1] & p.zero);
+          const uint32_t pos = (tt - a) * RP + h + NS;         // the tile sequence position to fetch
+          if (pos < ntiles) fetch_ahead(st, dep, (h + NS) / RP, (h + NS) % RP, true, oi, rt, kt, left, opk);
+          const __half* x_hi = (xrow && h == 0) ? xl + kt * kTileCols + 32 : nullptr;
+          const __half* x_next = h == RP - 1 ? x_nx : nullptr;
+          tile_body<MODE, C, L, TB, REPS, false, false, true>(cur, laneoff, mulk, xb, acc[h], nullptr, 0, x_hi, x_next,
+                                                             0u);
+          if (++st == NS) { st = 0; par ^= 1u; }
+        }
         --left;
         ++kt;
       }
@@ -389,66 +412,72 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     const bool row_end = run_row_end;
     const bool op_end = row_end && left == 0u;
     if (row_end || t == b) {
-      // ---- end of this warp's segment of row tile rt ----
+      // ---- end of this warp's segment of row group rt: each of its RP row tiles ----
       const int oe = opaque(oi);
       const int d_out = p.op[oe].d_out;
-      if (seg_k0 == 0 && row_end) {          // the whole row tile: store directly
-        void* yv = p.op[oe].y;
 #pragma unroll
-        for (int m = 0; m < 2; ++m)
+      for (int h = 0; h < RP; ++h) {
+        const uint32_t rth = RP * rt + h;                   // row tile
+        if (seg_k0 == 0 && row_end) {                       // the whole row tile: store directly
+          void* yv = p.op[oe].y;
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-            if (bb < p.batch) {
-              const float v = acc[m][r] * sc[2 * m + (r >> 1)];
-              const size_t e = (size_t)bb * d_out + rt * kTileRows + row;
-              if (p.y_f32) {
-                float* y = reinterpret_cast<float*>(yv) + e;
-                *y = p.y_accum ? *y + v : v;
-              } else {
-                reinterpret_cast<__half*>(yv)[e] = __float2half_rn(v);
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
+              if (bb < p.batch) {
+                const float v = acc[h][m][r] * sc[h][2 * m + (r >> 1)];
+                const size_t e = (size_t)bb * d_out + rth * kTileRows + row;
+                if (p.y_f32) {
+                  float* y = reinterpret_cast<float*>(yv) + e;
+                  *y = p.y_accum ? *y + v : v;
+                } else {
+                  reinterpret_cast<__half*>(yv)[e] = __float2half_rn(v);
+                }
               }
             }
-          }
-      } else {
-        float* wsb = p.op[oe].ws + rt * kTileRows;
+        } else {
+          float* wsb = p.op[oe].ws + rth * kTileRows;
 #pragma unroll
-        for (int m = 0; m < 2; ++m)
+          for (int m = 0; m < 2; ++m)
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-            if (bb < p.batch) atomicAdd(wsb + (size_t)bb * d_out + row, acc[m][r] * sc[2 * m + (r >> 1)]);
-          }
-        const int nk = (int)kt - seg_k0 + 1;
-        unsigned* cnt = reinterpret_cast<unsigned*>(p.op[oe].counters + rt);
-        __syncwarp();
-        int done = 0;
-        if (lane == 0) done = atom_add_acqrel(cnt, (unsigned)nk) + (unsigned)nk == KT;
-        done = __shfl_sync(0xffffffffu, done, 0);
-        if (done) {
-          // every k tile of row tile rt is in the workspace: write y, re-zero the workspace
-          __syncwarp();
-          void* yv = p.op[oe].y;
-          for (int e = lane; e < kTileRows * p.batch; e += 32) {
-            const int bb = e >> 5, row = e & 31;
-            float* wp = wsb + (size_t)bb * d_out + row;
-            const float v = __ldcg(wp);
-            __stcg(wp, 0.f);
-            const size_t ye = (size_t)bb * d_out + rt * kTileRows + row;
-            if (p.y_f32) {
-              float* y = reinterpret_cast<float*>(yv) + ye;
-              *y = p.y_accum ? *y + v : v;
-            } else {
-              reinterpret_cast<__half*>(yv)[ye] = __float2half_rn(v);
+            for (int r = 0; r < 4; ++r) {
+              const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
+              if (bb < p.batch) atomicAdd(wsb + (size_t)bb * d_out + row, acc[h][m][r] * sc[h][2 * m + (r >> 1)]);
             }
+          const int nk = (int)kt - seg_k0 + 1;
+          unsigned* cnt = reinterpret_cast<unsigned*>(p.op[oe].counters + rth);
+          __syncwarp();
+          int done = 0;
+          if (lane == 0) done = atom_add_acqrel(cnt, (unsigned)nk) + (unsigned)nk == KT;
+          done = __shfl_sync(0xffffffffu, done, 0);
+          if (done) {
+            // every k tile of row tile rth is in the workspace: write y, re-zero the workspace
+            __syncwarp();
+            void* yv = p.op[oe].y;
+            for (int e = lane; e < kTileRows * p.batch; e += 32) {
+              const int bb = e >> 5, row = e & 31;
+              float* wp = wsb + (size_t)bb * d_out + row;
+              const float v = __ldcg(wp);
+              __stcg(wp, 0.f);
+              const size_t ye = (size_t)bb * d_out + rth * kTileRows + row;
+              if (p.y_f32) {
+                float* y = reinterpret_cast<float*>(yv) + ye;
+                *y = p.y_accum ? *y + v : v;
+              } else {
+                reinterpret_cast<__half*>(yv)[ye] = __float2half_rn(v);
+              }
+            }
+            if (lane == 0) st_relaxed(cnt, 0u);
           }
-          if (lane == 0) st_relaxed(cnt, 0u);
         }
       }
 #pragma unroll
-      for (int m = 0; m < 2; ++m)
+      for (int h = 0; h < RP; ++h)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) acc[m][r] = 0.f;
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) acc[h][m][r] = 0.f;
       seg_k0 = 0;
     }
     // ---- advance to the next run ----
@@ -461,7 +490,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
         if (t < b) {
           const int on = opaque(oi);
           opk = pack(on);
-          left = (uint32_t)p.op[on].RT * p.op[on].KT;
+          left = units_of(on);
           enter_op(on);
           xl = xlane(on);
           if (xrow) {
@@ -507,7 +536,15 @@ struct EngineVariant {
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    auto k = qp_engine_kernel<MODE, L, TB, REPS, CMIN, CMAX>;
+    // row pairs only for the small-table schemes: the TCQ decode is register-bound, and a second set of
+    // accumulators + scales cost more than the halved activation loads save (measured: C2 at batch 4
+    // +32%, batch 8 +12%; VQ-3 / NUQ-4 at batch 8 -9%, profiles/r2/ab_rp.md)
+    void (*k)(EngParams) = qp_engine_kernel<MODE, L, TB, REPS, CMIN, CMAX, 1>;
+    if constexpr (MODE == DEC_LUT2) {
+      if (prm.rp == 2) k = qp_engine_kernel<MODE, L, TB, REPS, CMIN, CMAX, 2>;
+    } else {
+      prm.rp = 1;
+    }
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PL::SMEM_MAX);
     if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k, prm);
     return e;

@@ -1129,6 +1129,14 @@ bool same_table(const qp_codebook* a, const qp_codebook* b) {
   return a == b || (a->mode == b->mode && a->L == b->L && a->tb == b->tb && a->reps == b->reps &&
                     a->table_words == b->table_words && a->host == b->host);
 }
+int eng_rp_min_batch() {   // QP_ENG_RP2_MIN_BATCH: smallest batch for row-pair units (9 = never)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QP_ENG_RP2_MIN_BATCH");
+    v = e ? atoi(e) : 4;
+  }
+  return v;
+}
 int eng_late_stages() {   // QP_ENG_LATE=1: fill ring stages 1.. only once x' is ready (experiment)
   static int v = -1;
   if (v < 0) {
@@ -1268,6 +1276,12 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
     p.y_accum = (flags & QP_Y_ACCUMULATE) ? 1 : 0;
     p.table = m->layers[gr.first]->cb->d_table;
     p.gen = gr.d_gen;
+    // row-pair units (two row tiles per k tile share the activation fragments) from batch 4 on,
+    // when every layer of the launch has an even number of row tiles
+    int rp = batch >= eng_rp_min_batch() && m->layers[gr.first]->cb->mode == DEC_LUT2 ? 2 : 1;
+    for (int k = 0; k < gr.n; ++k)
+      if ((m->layers[gr.first + k]->d_out / kTileRows) % 2) rp = 1;
+    p.rp = rp;
     uint32_t tiles = 0;
     int jobs = 0, scratch = 0;
     for (int k = 0; k < gr.n; ++k) {
@@ -1285,7 +1299,7 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
       o.d_in = l->d_in;
       o.d_out = l->d_out;
       o.tile0 = tiles;
-      tiles += (uint32_t)(o.RT * o.KT);
+      tiles += (uint32_t)((o.RT / rp) * o.KT);
       o.x_raw = xs[i];
       o.xr = pre ? static_cast<__half*>(const_cast<void*>(xs[i])) : m->d_xr[i];
       o.rht_signs = l->rht->d_signs;
@@ -1307,7 +1321,7 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
     // CTA ranges over the flat tile order; the CTAs that run rotation jobs take job_tiles fewer
     // tiles per job
     const uint32_t S = tiles;
-    const double jt = eng_job_tiles();
+    const double jt = eng_job_tiles() / rp;
     const double base = ((double)S + jt * jobs) / grid;
     double acc = 0;
     p.cta_begin[0] = 0;

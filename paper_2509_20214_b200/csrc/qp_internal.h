@@ -113,7 +113,7 @@ struct EngOp {
   int RT, KT, KH;              // row tiles, k tiles, k tiles at c_lo
   int c_lo, c_hi;              // bits per step
   int d_in, d_out;
-  uint32_t tile0;              // first engine-wide tile index of this layer (prefix sum)
+  uint32_t tile0;              // first engine-wide work unit of this layer (prefix sum; units = RT/rp * KT)
   // rotation: njobs = batch * d_in / rht_block jobs [job0, job0 + njobs), or 0 when x
   // is already x' (xr = x)
   const void* x_raw;
@@ -138,10 +138,11 @@ struct EngParams {
   int ns;                      // ring stages per warp (set by the launcher)
   int rot_scratch_bytes;       // shared memory the rotation jobs need (b_max * 4)
   int late_stages;             // 1: ring stages 1.. are first filled after the layer's x' is ready
+  int rp;                      // row tiles per work unit (1, or 2 = row pairs sharing the activations)
   uint32_t zero;               // always 0 (an operand the compiler cannot fold)
   const uint32_t* table;       // compact decode table shared by every layer
   unsigned* gen;               // [1]: CTAs out this launch (the last one resets the ready counters)
-  uint32_t cta_begin[kMaxEngCtas + 1];   // CTA c owns tiles [cta_begin[c], cta_begin[c+1])
+  uint32_t cta_begin[kMaxEngCtas + 1];   // CTA c owns units [cta_begin[c], cta_begin[c+1])
   EngOp op[kMaxEngOps];
 };
 
