@@ -1129,6 +1129,14 @@ bool same_table(const qp_codebook* a, const qp_codebook* b) {
   return a == b || (a->mode == b->mode && a->L == b->L && a->tb == b->tb && a->reps == b->reps &&
                     a->table_words == b->table_words && a->host == b->host);
 }
+bool eng_single() {   // QP_ENG_SINGLE=1: one-layer groups through the engine too (experiments)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("QP_ENG_SINGLE");
+    v = (e && atoi(e) != 0) ? 1 : 0;
+  }
+  return v == 1;
+}
 int eng_rp_min_batch() {   // QP_ENG_RP2_MIN_BATCH: smallest batch for row-pair units (9 = never)
   static int v = -1;
   if (v < 0) {
@@ -1192,7 +1200,10 @@ extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_mu
       }
     }
     gr.n = j - i;
-    gr.launch = f;
+    // a single layer runs faster through the per-layer path (the rotation kernel under PDL overlaps
+    // the GEMV's prologue; one-layer engine launches pay the in-kernel rotation handoff and split-K
+    // flushes on < 1 tile per warp): 4096^2 TCQ-2.5 9.0 vs 10.4 us at batch 1 (profiles/r2/one_layer.md)
+    gr.launch = (gr.n == 1 && !eng_single()) ? nullptr : f;
     m->groups.push_back(gr);
     i = j;
   }
