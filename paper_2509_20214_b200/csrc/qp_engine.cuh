@@ -163,6 +163,7 @@ __device__ __forceinline__ void c_dispatch(int c, F&& f) {
 #ifdef QP_ENG_TIMELINE
 // experiment builds only (-DQP_ENG_TIMELINE): globaltimer stamps of warp 0 of every CTA
 __device__ unsigned long long g_eng_tl[kMaxEngCtas][8];
+__device__ unsigned long long g_eng_wl[kMaxEngCtas][16];   // per-warp main-loop end
 #define QP_TL(k) do { if (threadIdx.x == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_eng_tl[blockIdx.x][k] = t_; } } while (0)
 #else
 #define QP_TL(k) do { } while (0)
@@ -505,6 +506,13 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     }
   }
   QP_TL(5);
+#ifdef QP_ENG_TIMELINE
+  if (lane == 0 && warp < 16) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    g_eng_wl[blockIdx.x][warp] = t_;
+  }
+#endif
   asm volatile("griddepcontrol.launch_dependents;");
   // the last CTA out resets the launch's ready counters (every CTA is past its waits)
   __syncthreads();

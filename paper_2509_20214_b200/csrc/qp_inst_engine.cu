@@ -23,8 +23,11 @@ struct Register {
 // experiment builds (-DQP_ENG_TIMELINE): copy the per-CTA stamps of the last engine launch
 extern "C" int qp_debug_engine_timeline(unsigned long long* host, int n) {
 #ifdef QP_ENG_TIMELINE
-  if (n > kMaxEngCtas * 8) n = kMaxEngCtas * 8;
-  return (int)cudaMemcpyFromSymbol(host, g_eng_tl, (size_t)n * 8);
+  if (n > kMaxEngCtas * 24) n = kMaxEngCtas * 24;
+  const int n1 = n < kMaxEngCtas * 8 ? n : kMaxEngCtas * 8;
+  cudaError_t e = cudaMemcpyFromSymbol(host, g_eng_tl, (size_t)n1 * 8);
+  if (e == cudaSuccess && n > n1) e = cudaMemcpyFromSymbol(host + n1, g_eng_wl, (size_t)(n - n1) * 8);
+  return (int)e;
 #else
   (void)host;
   (void)n;

@@ -35,6 +35,17 @@ SETS = {
 }
 
 
+def c4_sets():
+    """C4 (Llama-3.1-70B MLP, row-sharded at P = 1/2/4/8): rank 0's shards of gate / up (28672 x 8192)
+    and down (8192 x 28672) as one engine launch -- the per-rank compute of the sharded step (the
+    all-gather needs more than one GPU)."""
+    out = {}
+    for P in (1, 2, 4, 8):
+        for s_, x4 in (("tcq", 10), ("tcq", 16), ("vq", 12), ("nuq", 16)):
+            out[f"c4:p{P}:{s_}:{x4}"] = [(28672 // P, 8192, s_, x4), (28672 // P, 8192, s_, x4), (8192 // P, 28672, s_, x4)]
+    return out
+
+
 def palette_sets():
     """C3 through the engine: every target quantizer (2-4.5 bits) over the three C2 shapes, one
     engine launch per set (the 3 layers of one quantizer share its decode table)."""
@@ -53,12 +64,16 @@ def main():
     ap.add_argument("--prerotated", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph (for ncu)")
     ap.add_argument("--palette", action="store_true", help="C3: every target quantizer over the C2 shapes")
+    ap.add_argument("--c4", action="store_true", help="C4: 70B MLP row shards at P = 1/2/4/8 (rank 0)")
     ap.add_argument("--batches", default="")
     ap.add_argument("--per-layer", action="store_true", help="qp_linear_fwd per layer instead of qp_multi_fwd")
     args = ap.parse_args()
     if args.palette:
         SETS.update(palette_sets())
         args.sets = ",".join(k for k in SETS if k.startswith("c3:"))
+    if args.c4:
+        SETS.update(c4_sets())
+        args.sets = ",".join(k for k in SETS if k.startswith("c4:"))
     import torch
     from paper_2509_20214_b200 import _lib as QL
     from qp_synth import activations_fp16, channel_scales, random_code_bytes

@@ -54,8 +54,10 @@ def main():
             m, xs, ys, _ = reps[it % 3]
             m.forward(xs, 1, ys, flags=flags)
         torch.cuda.synchronize()
-        buf = np.zeros((192, 8), dtype=np.uint64)
-        assert fn(buf.ctypes.data, buf.size) == 0
+        allb = np.zeros(192 * 24, dtype=np.uint64)
+        assert fn(allb.ctypes.data, allb.size) == 0
+        buf = allb[:192 * 8].reshape(192, 8)
+        wl = allb[192 * 8:].reshape(192, 16)
         g = 148
         t = buf[:g].astype(np.int64)
         t0 = t[:, 0].min()
@@ -70,6 +72,11 @@ def main():
             print(f"  {nm:10s} n={len(v):3d}  {rel.min():7.2f} {statistics.median(rel):7.2f} {rel.max():7.2f}")
         le = (t[:, 5] - t0) / 1e3
         print("  loop_end per CTA (us):", " ".join(f"{v:.0f}" for v in le))
+        w = (wl[:g].astype(np.int64) - t0) / 1e3                       # [cta][warp]
+        rel = w - w.mean(axis=1, keepdims=True)
+        print("  per-warp loop end minus the CTA mean (us), averaged over CTAs, warps 0..15:")
+        print("   ", " ".join(f"{v:+.2f}" for v in rel.mean(axis=0)))
+        print("  spread within a CTA (max - min), median over CTAs: %.2f us" % np.median(w.max(1) - w.min(1)))
 
 
 if __name__ == "__main__":
