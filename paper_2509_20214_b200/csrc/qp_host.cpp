@@ -1129,11 +1129,11 @@ bool same_table(const qp_codebook* a, const qp_codebook* b) {
   return a == b || (a->mode == b->mode && a->L == b->L && a->tb == b->tb && a->reps == b->reps &&
                     a->table_words == b->table_words && a->host == b->host);
 }
-bool eng_single() {   // QP_ENG_SINGLE=1: one-layer groups through the engine too (experiments)
+bool eng_single() {   // QP_ENG_SINGLE=0: one-layer groups through the per-layer path (experiments)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("QP_ENG_SINGLE");
-    v = (e && atoi(e) != 0) ? 1 : 0;
+    v = e ? (atoi(e) != 0 ? 1 : 0) : 1;
   }
   return v == 1;
 }
@@ -1200,9 +1200,8 @@ extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_mu
       }
     }
     gr.n = j - i;
-    // a single layer runs faster through the per-layer path (the rotation kernel under PDL overlaps
-    // the GEMV's prologue; one-layer engine launches pay the in-kernel rotation handoff and split-K
-    // flushes on < 1 tile per warp): 4096^2 TCQ-2.5 9.0 vs 10.4 us at batch 1 (profiles/r2/one_layer.md)
+    // (QP_ENG_SINGLE=0: one-layer groups through the per-layer path instead -- faster for one layer
+    // launched back to back, slower inside a mixed sequence such as C5: profiles/r2/one_layer.md)
     gr.launch = (gr.n == 1 && !eng_single()) ? nullptr : f;
     m->groups.push_back(gr);
     i = j;

@@ -150,15 +150,15 @@ def test_engine_repeated_launches_graph_and_accumulate():
 
 
 def test_engine_mixed_tables_and_fallback():
-    """Layers of different decode tables split into several launch groups: the engine for runs of
-    >= 2 layers with a variant (TCQ tb = 9, VQ-3), the per-layer path for single layers (NUQ-4,
-    TCQ-2.0 between other tables) and layers without a variant (UNIF-8 / DEC_SCALAR, TCQ-5.0)."""
+    """Layers of different decode tables split into several launch groups: the engine where a
+    variant exists (TCQ tb = 9 twice, VQ-3, NUQ-4), the per-layer path for layers without one
+    (UNIF-8 / DEC_SCALAR, TCQ-5.0)."""
     Lb = _lib()
     specs = [(160, 1536, "tcq", 10), (96, 1024, "tcq", 16), (128, 2048, "vq", 12), (64, 1024, "vq", 12),
              (96, 1536, "nuq", 16), (64, 512, "unif", 32), (32, 1024, "tcq", 20), (64, 768, "tcq", 8)]
     items = _make(specs, first_id=100)
     m = Lb.Multi([it[0] for it in items])
-    assert m.n_launches == 6 and m.n_engine_launches == 2
+    assert m.n_launches == 6 and m.n_engine_launches == 4
     batch = 3
     xs_np = [activations_fp16(batch, it[0].d_in, seed=41 + i) for i, it in enumerate(items)]
     xs = [torch.from_numpy(x).cuda() for x in xs_np]
