@@ -1141,7 +1141,7 @@ int eng_rp_min_batch() {   // QP_ENG_RP2_MIN_BATCH: smallest batch for row-pair 
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("QP_ENG_RP2_MIN_BATCH");
-    v = e ? atoi(e) : 4;
+    v = e ? atoi(e) : 8;
   }
   return v;
 }
@@ -1288,9 +1288,18 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
     p.gen = gr.d_gen;
     // row-pair units (two row tiles per k tile share the activation fragments) from batch 4 on,
     // when every layer of the launch has an even number of row tiles
+    // -- and only with >= 8 row-pair units per warp: coarser units cost balance on small launches
+    // (C3's three layers per launch: +7% at batch 4; the 9-layer sets: -9% at batch 8; ab_rp.md)
     int rp = batch >= eng_rp_min_batch() && m->layers[gr.first]->cb->mode == DEC_LUT2 ? 2 : 1;
-    for (int k = 0; k < gr.n; ++k)
-      if ((m->layers[gr.first + k]->d_out / kTileRows) % 2) rp = 1;
+    {
+      long long tiles_all = 0;
+      for (int k = 0; k < gr.n; ++k) {
+        const qp_layer* l = m->layers[gr.first + k];
+        if ((l->d_out / kTileRows) % 2) rp = 1;
+        tiles_all += (long long)(l->d_out / kTileRows) * (l->d_in / kTileCols);
+      }
+      if (tiles_all / 2 < 8LL * 16 * std::min(num_sms(), kMaxEngCtas)) rp = 1;
+    }
     p.rp = rp;
     uint32_t tiles = 0;
     int jobs = 0, scratch = 0;
