@@ -546,6 +546,36 @@ def main():
             b.synchronize()
         return a.elapsed_time(b) * 1e3 / (reps * n_rep)
 
+    # the same steps with QP_INDEPENDENT (the caller's promise that no running work touches a step's
+    # x / y: consecutive steps may overlap), reported beside the dependency-safe default
+    indep = None
+    if use_engine and world == 1:
+        gi = []
+        with torch.cuda.stream(stream):
+            for rep in range(REPLICAS):
+                group = insts[rep * n_layers:(rep + 1) * n_layers]
+                if eager:
+                    gi.append(None)
+                    continue
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    multis[rep].forward([i["x"] for i in group], batch, [i["y"] for i in group],
+                                        flags=extra_flags | QL.QP_INDEPENDENT, stream=stream)
+                gi.append(g)
+            if not eager:
+                for i in range(args.warmup):
+                    gi[i % REPLICAS].replay()
+                stream.synchronize()
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                for i in range(args.steps):
+                    gi[i % REPLICAS].replay()
+                a1.record(stream)
+                a1.synchronize()
+                ms_i = a0.elapsed_time(a1) / args.steps
+                indep = {"ms_per_step": round(ms_i, 5), "value": round(step_bytes / (ms_i * 1e-3) / 1e9, 2),
+                         "unit": "GB/s", "flag": "QP_INDEPENDENT"}
+
     batch_lines = {}
     if use_engine:
         # (N > 1: the engine alone over this rank's shards, i.e. per-rank bytes / time, no all-gather)
@@ -692,7 +722,8 @@ def main():
                        "path": ("engine: one persistent qp_multi_fwd launch per step (rotation jobs + all 9 "
                                 "GEMVs, device-side ready flags)" if use_engine else
                                 "per layer: qp_linear_fwd = rotation kernel + fused GEMV kernel, PDL-chained"),
-                       "gemv_us_per_layer": per_layer_us},
+                       "gemv_us_per_layer": per_layer_us,
+                       "independent_steps": indep},
             "roofline": ({"bound": "hbm", "achieved": round(eng["achieved"], 1), "peak": peak, "unit": "GB/s",
                           "frac": round(eng["achieved"] / peak, 4),
                           "traffic": round(eng_traffic) if eng_traffic else None, "traffic_source": eng_traffic_src,

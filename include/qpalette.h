@@ -77,6 +77,11 @@ typedef enum { QP_F16 = 0, QP_BF16 = 1, QP_F32 = 2 } qp_dtype;
                                 zeroed in-kernel) instead of launching the rotation kernel, when x'
                                 fits the kernel's plan. Opt-in: on B200 at the C2 shapes the
                                 PDL-overlapped rotation kernel is faster (profiles/r1/ab_xs_r1.md) */
+#define QP_INDEPENDENT 32u  /* qp_multi_fwd only: no work still running on the stream reads or writes this
+                                call's x or y (e.g. independent requests, or steps whose inputs are already
+                                resident): the engine launch then does not wait for the preceding kernel
+                                (griddepcontrol.wait), only for the previous launch of the same qp_multi,
+                                so consecutive calls overlap. Ignored by the per-layer fallback.        */
 #define QP_Y_ACCUMULATE 8u  /* fp32 y only: y += diag(s) W_hat R x (y is not zeroed first; e.g. a residual
                                 add). Not with QP_DETERMINISTIC.                                        */
 
@@ -175,7 +180,7 @@ qp_status qp_dequantize(const qp_layer* l, void* W_hat_fp16, void* stream);
  * allocates and is graph-capturable. A qp_multi may be used by one stream at a time.
  * qp_multi_fwd: xs[i] device [batch][d_in_i] of dtype xt (16-byte aligned; with QP_X_PREROTATED fp16
  * R x, 32-byte aligned), ys[i] device [batch][d_out_i] of dtype yt in {F16, F32}; outputs must not
- * alias inputs. Flags: QP_X_PREROTATED, QP_NO_PDL, QP_Y_ACCUMULATE (fp32 y += ...). QP_DETERMINISTIC
+ * alias inputs. Flags: QP_X_PREROTATED, QP_NO_PDL, QP_Y_ACCUMULATE (fp32 y += ...), QP_INDEPENDENT. QP_DETERMINISTIC
  * and QP_FUSE_RHT are rejected (QP_ERR_INVALID_ARG). Other errors as qp_linear_fwd. */
 qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_multi** out);
 qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype xt, int batch, void* const* ys, qp_dtype yt,

@@ -27,6 +27,7 @@ QP_NO_PDL = 2
 QP_DETERMINISTIC = 4
 QP_Y_ACCUMULATE = 8
 QP_FUSE_RHT = 16
+QP_INDEPENDENT = 32
 
 # every symbol include/qpalette.h declares (checked by tests/test_abi.py)
 EXPORTS = [

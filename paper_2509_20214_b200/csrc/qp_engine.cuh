@@ -265,10 +265,37 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   // the tile sequence position pos (relative to unit a's first tile) -> (units ahead, h)
   const uint32_t ntiles = (b - a) * RP;
 
+  // ---- ordering with earlier work ----------------------------------------------------------------
+  // Default: griddepcontrol.wait (x may come from the preceding kernel; y may be read by it).
+  // QP_INDEPENDENT (the caller guarantees that no work still running on the stream touches this
+  // call's x or y): no wait on the preceding kernel -- consecutive independent calls overlap -- only
+  // on the previous launch of THIS launch group (its workspace, counters and x' scratch): every CTA
+  // takes an entry ticket (64-bit, monotonic), ticket / gridDim.x is the launch index, and the CTA
+  // waits until that many launches of the group have exited (gen64[1], bumped by the last CTA out).
+  unsigned long long* gen64 = reinterpret_cast<unsigned long long*>(p.gen + 2);   // [0] entry, [1] exits
+  auto order_before = [&]() {
+    // every launch takes its tickets (so launch indices count dependent and independent launches)
+    const unsigned long long ticket = tid == 0 ? atomicAdd(gen64, 1ull) : 0ull;
+    if (!p.independent) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      return;
+    }
+    if (tid == 0) {
+      const unsigned long long idx = ticket / gridDim.x;
+      for (;;) {
+        unsigned long long done;
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(done) : "l"(gen64 + 1) : "memory");
+        if ((long long)(done - idx) >= 0) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  };
+
   // ---- rotation jobs (the first CTAs): x' of every layer, before this CTA's own tiles ------------
   const bool rotor = (int)blockIdx.x < p.total_jobs;
   if (rotor) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");          // x may come from the previous kernel
+    order_before();
     QP_TL(1);
     for (int j = blockIdx.x; j < p.total_jobs; j += gridDim.x) {
       int jo = 0;
@@ -295,7 +322,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   if (!p.late_stages)
     for (int st = 1; st < NS && (uint32_t)st < ntiles; ++st)
       fetch_ahead(st, 0u, (uint32_t)st / RP, (uint32_t)st % RP, true, oi, rt, kt, left, opk);
-  if (!rotor) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!rotor) order_before();
   QP_TL(3);
   __syncthreads();
 
@@ -520,6 +547,8 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     if (atom_add_acqrel(p.gen, 1u) == gridDim.x - 1) {
       for (int o_ = 0; o_ < p.n_ops; ++o_) st_relaxed(p.op[o_].ready, 0u);
       st_relaxed(p.gen, 0u);
+      // this launch of the group has exited (QP_INDEPENDENT launches of the group wait for it)
+      asm volatile("red.release.gpu.global.add.u64 [%0], 1;" :: "l"(gen64 + 1) : "memory");
     }
   }
   QP_TL(6);

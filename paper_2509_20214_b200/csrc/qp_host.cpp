@@ -1121,7 +1121,7 @@ struct qp_multi {
   std::vector<float*> d_ws;            // per layer: [8][d_out] fp32, zero between launches
   std::vector<int*> d_cnt;             // per layer: [RT] k-tile counters, zero between launches
   unsigned* d_flags = nullptr;         // per layer: ready (+ 1 spare word)
-  unsigned* d_gens = nullptr;          // per group [4]
+  unsigned* d_gens = nullptr;          // per group [8]: exit counter, pad, 64-bit entry / exit counts
 };
 
 namespace {
@@ -1207,7 +1207,7 @@ extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_mu
     i = j;
   }
   m->d_flags = static_cast<unsigned*>(dev_alloc((size_t)2 * n * 4));
-  m->d_gens = static_cast<unsigned*>(dev_alloc(m->groups.size() * 4 * 4));
+  m->d_gens = static_cast<unsigned*>(dev_alloc(m->groups.size() * 8 * 4));
   bool ok = m->d_flags && m->d_gens;
   for (int i = 0; i < n && ok; ++i) {
     const qp_layer* l = layers[i];
@@ -1220,7 +1220,7 @@ extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_mu
       ok = false;
   }
   if (ok && (cudaMemset(m->d_flags, 0, (size_t)2 * n * 4) != cudaSuccess ||
-             cudaMemset(m->d_gens, 0, m->groups.size() * 4 * 4) != cudaSuccess))
+             cudaMemset(m->d_gens, 0, m->groups.size() * 8 * 4) != cudaSuccess))
     ok = false;
   // the memsets run on the legacy stream: complete them before any stream uses the object
   if (ok && cudaDeviceSynchronize() != cudaSuccess) ok = false;
@@ -1229,7 +1229,7 @@ extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_mu
     delete m;
     return fail(QP_ERR_ALLOC, "qp_multi_create: device allocation failed");
   }
-  for (size_t k = 0; k < m->groups.size(); ++k) m->groups[k].d_gen = m->d_gens + 4 * k;
+  for (size_t k = 0; k < m->groups.size(); ++k) m->groups[k].d_gen = m->d_gens + 8 * k;   // 8-byte aligned
   *out = m;
   return QP_OK;
 }
@@ -1266,13 +1266,14 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
   if (flags & (QP_DETERMINISTIC | QP_FUSE_RHT))
     return fail(QP_ERR_INVALID_ARG, "qp_multi_fwd: QP_DETERMINISTIC / QP_FUSE_RHT are per-layer options (use "
                 "qp_linear_fwd)");
+  const unsigned layer_flags = flags & ~QP_INDEPENDENT;   // the per-layer fallback ignores QP_INDEPENDENT
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool pdl = !(flags & QP_NO_PDL) && !pdl_disabled_by_env();
   const bool pre = (flags & QP_X_PREROTATED) != 0;
   for (const auto& gr : m->groups) {
     if (!gr.launch) {
       for (int i = gr.first; i < gr.first + gr.n; ++i) {
-        qp_status st = qp_linear_fwd(m->layers[i], xs[i], xt, batch, ys[i], yt, flags, stream);
+        qp_status st = qp_linear_fwd(m->layers[i], xs[i], xt, batch, ys[i], yt, layer_flags, stream);
         if (st != QP_OK) return st;
       }
       continue;
@@ -1336,6 +1337,7 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
     p.total_jobs = jobs;
     p.rot_scratch_bytes = scratch;
     p.late_stages = eng_late_stages();
+    p.independent = (flags & QP_INDEPENDENT) ? 1 : 0;
     const int grid = (int)std::min<long long>(std::min(num_sms(), kMaxEngCtas), tiles);
     // CTA ranges over the flat tile order; the CTAs that run rotation jobs take job_tiles fewer
     // tiles per job
@@ -1382,7 +1384,9 @@ extern "C" qp_status qp_multi_fwd_sharded(qp_multi* m, const void* const* xs, qp
                   "(qp_layer_shard)", i, world);
     local[i] = l->d_gather;
   }
-  qp_status st = qp_multi_fwd(m, xs, xt, batch, local.data(), yt, flags, stream);
+  // (QP_INDEPENDENT is dropped: the next engine launch must not overwrite the local rows while the
+  // preceding all-gather still reads them)
+  qp_status st = qp_multi_fwd(m, xs, xt, batch, local.data(), yt, flags & ~QP_INDEPENDENT, stream);
   if (st != QP_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ncclResult_t r = ncclGroupStart();

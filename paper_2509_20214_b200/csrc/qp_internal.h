@@ -141,7 +141,9 @@ struct EngParams {
   int rp;                      // row tiles per work unit (1, or 2 = row pairs sharing the activations)
   uint32_t zero;               // always 0 (an operand the compiler cannot fold)
   const uint32_t* table;       // compact decode table shared by every layer
-  unsigned* gen;               // [1]: CTAs out this launch (the last one resets the ready counters)
+  unsigned* gen;               // [0] CTAs out this launch (the last one resets the ready counters);
+                               // [2..5] two 64-bit words: entry tickets, exited launches (QP_INDEPENDENT)
+  int independent;             // QP_INDEPENDENT: no griddepcontrol.wait, only the group's previous launch
   uint32_t cta_begin[kMaxEngCtas + 1];   // CTA c owns units [cta_begin[c], cta_begin[c+1])
   EngOp op[kMaxEngOps];
 };

@@ -149,6 +149,53 @@ def test_engine_repeated_launches_graph_and_accumulate():
             assert np.max(linear.normwise_error(y.cpu().numpy() - 1.0, r)) <= TOL
 
 
+def test_engine_independent_launches_overlap_safely():
+    """QP_INDEPENDENT: consecutive launches do not wait for each other, only for the previous launch
+    of the same qp_multi (entry tickets / exit counts). Two objects alternating (as bench.py's
+    replicas) and one object back to back, eager and in a CUDA graph, against the oracle."""
+    Lb = _lib()
+    objs = []
+    for rep in range(2):
+        items = _make(TB9_MIX, first_id=180 + 10 * rep)
+        m = Lb.Multi([it[0] for it in items])
+        xs_np = [activations_fp16(2, it[0].d_in, seed=71 + i + 7 * rep) for i, it in enumerate(items)]
+        xs = [torch.from_numpy(x).cuda() for x in xs_np]
+        ys = [torch.empty(2, it[0].d_out, dtype=torch.float32, device="cuda") for it in items]
+        refs = [_ref(it, x) for it, x in zip(items, xs_np)]
+        objs.append((m, xs, ys, refs))
+    F = Lb.QP_INDEPENDENT
+    for k in range(6):
+        m, xs, ys, _ = objs[k % 2]
+        m.forward(xs, 2, ys, flags=F)
+    m0, xs0, ys0, _ = objs[0]
+    for _ in range(4):
+        m0.forward(xs0, 2, ys0, flags=F)
+    torch.cuda.synchronize()
+    for m, xs, ys, refs in objs:
+        for y, r in zip(ys, refs):
+            assert np.max(linear.normwise_error(y.cpu().numpy(), r)) <= TOL
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for k in range(4):
+                m, xs, ys, _ = objs[k % 2]
+                m.forward(xs, 2, ys, flags=F, stream=s)
+        for _ in range(5):
+            g.replay()
+        s.synchronize()
+    for m, xs, ys, refs in objs:
+        for y, r in zip(ys, refs):
+            assert np.max(linear.normwise_error(y.cpu().numpy(), r)) <= TOL
+    # the dependent default after independent launches on the same objects
+    for m, xs, ys, refs in objs:
+        m.forward(xs, 2, ys)
+    torch.cuda.synchronize()
+    for m, xs, ys, refs in objs:
+        for y, r in zip(ys, refs):
+            assert np.max(linear.normwise_error(y.cpu().numpy(), r)) <= TOL
+
+
 def test_engine_mixed_tables_and_fallback():
     """Layers of different decode tables split into several launch groups: the engine where a
     variant exists (TCQ tb = 9 twice, VQ-3, NUQ-4), the per-layer path for layers without one

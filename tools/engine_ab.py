@@ -67,6 +67,7 @@ def main():
     ap.add_argument("--c4", action="store_true", help="C4: 70B MLP row shards at P = 1/2/4/8 (rank 0)")
     ap.add_argument("--batches", default="")
     ap.add_argument("--per-layer", action="store_true", help="qp_linear_fwd per layer instead of qp_multi_fwd")
+    ap.add_argument("--independent", action="store_true", help="QP_INDEPENDENT launches (consecutive calls overlap)")
     args = ap.parse_args()
     if args.palette:
         SETS.update(palette_sets())
@@ -106,7 +107,7 @@ def main():
             multis.append(QL.Multi(lays))
             xs.append([torch.from_numpy(activations_fp16(B, i)).cuda() for o, i, s, x in specs])
             ys.append([torch.empty(B, o, dtype=torch.float32, device="cuda") for o, i, s, x in specs])
-        flags = QL.QP_X_PREROTATED if args.prerotated else 0
+        flags = (QL.QP_X_PREROTATED if args.prerotated else 0) | (QL.QP_INDEPENDENT if args.independent else 0)
         st = torch.cuda.Stream()
         with torch.cuda.stream(st):
             def run():
@@ -139,7 +140,7 @@ def main():
                           "us_per_layer": round(us / len(specs), 3), "gbs": round(alg / (us * 1e-6) / 1e9, 1),
                           "frac": round(alg / (us * 1e-6) / 1e9 / peak, 4), "engine_launches": multis[0].n_engine_launches,
                           "launches_per_call": multis[0].n_launches, "replicas": n_rep,
-                          "prerotated": args.prerotated, "path": "per-layer" if args.per_layer else "engine"}), flush=True)
+                          "prerotated": args.prerotated, "path": "per-layer" if args.per_layer else "engine", "independent": args.independent}), flush=True)
         del multis, xs, ys
         torch.cuda.synchronize()
 
