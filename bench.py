@@ -276,6 +276,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--allgather", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: p2p = the all-gather fused into the engine epilogue (peer stores over NVLink, "
+                         "qp_multi_fwd_sharded_p2p; default); nccl = engine + one grouped ncclAllGather")
     ap.add_argument("--path", default="engine", choices=["engine", "layer"],
                     help="engine: one persistent qp_multi_fwd launch per step (default); layer: qp_linear_fwd "
                          "per layer (rotation kernel + GEMV kernel each)")
@@ -359,6 +362,23 @@ def main():
         for rep in range(REPLICAS):
             multis.append(QL.Multi([inst["layer"] for inst in insts[rep * n_layers:(rep + 1) * n_layers]]))
 
+    # N > 1, fused all-gather: every replica's y_full buffers + flags, IPC-mapped across the ranks
+    pgs, allgather = [], args.allgather if (use_engine and world > 1) else None
+    if allgather == "p2p":
+        for rep in range(REPLICAS):
+            pgs.append(QL.MultiPeerGather(world, rank, [L["m"] for L in layers], batch, dtype=torch.float32))
+        # one checked round before timing: the fused path must reproduce the NCCL path's y_full
+        with torch.cuda.stream(torch.cuda.current_stream()):
+            group = insts[:n_layers]
+            multis[0].forward_sharded([i["x"] for i in group], batch, [i["y"] for i in group], comm)
+            pgs[0].forward(multis[0], [i["x"] for i in group])
+        torch.cuda.synchronize()
+        bad = max(float((pgs[0].ys[j] - insts[j]["y"]).abs().max() / insts[j]["y"].abs().max().clamp_min(1e-30))
+                  for j in range(n_layers))
+        if bad > 1e-4:
+            print(f"[bench] fused all-gather differs from the NCCL path ({bad:.2e}): using NCCL", file=sys.stderr)
+            allgather = "nccl"
+
     def fwd(inst, stream=None, flags=0):
         flags |= extra_flags
         if world > 1:
@@ -369,7 +389,11 @@ def main():
     def step_fn(rep, stream):
         """One step: the 9 layers of replica `rep` (rotation + fused dequant-GEMV each)."""
         group = insts[rep * n_layers:(rep + 1) * n_layers]
-        if use_engine and world > 1:
+        if use_engine and world > 1 and allgather == "p2p":
+            # this rank's shards through the engine, whose epilogue stores every final value into
+            # every rank's y_full (NVLink peer stores); one wait kernel for the deliveries
+            pgs[rep].forward(multis[rep], [i["x"] for i in group], flags=extra_flags, stream=stream)
+        elif use_engine and world > 1:
             # this rank's shards through the engine, then one grouped NCCL all-gather of all 9 outputs
             multis[rep].forward_sharded([i["x"] for i in group], batch, [i["y"] for i in group], comm,
                                         flags=extra_flags, stream=stream)
@@ -714,8 +738,10 @@ def main():
             "config": {"workload": "C2: Llama-3.1-8B (4096x4096, 14336x4096, 4096x14336) x TCQ-2.5 / half-TCQ-3.25 / "
                                    "TCQ-4.0 (L=16), rotation + fused dequant-GEMV per layer (qp_linear_fwd on raw x)",
                        "batch": batch, "layers_per_step": n_layers, "us_per_layer": round(ms * 1e3 / n_layers, 3),
-                       "parallelism": (f"row-shard x{world}: engine over each rank's shards + one grouped NCCL "
-                                       f"all-gather per step" if world > 1 else "single GPU"),
+                       "parallelism": ((f"row-shard x{world}: engine over each rank's shards with the all-gather "
+                                        f"fused into its epilogue (peer stores over NVLink)" if allgather == "p2p" else
+                                        f"row-shard x{world}: engine over each rank's shards + one grouped NCCL "
+                                        f"all-gather per step") if world > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (2 replicas, 326 MB per 2 steps, L2 126 MB)",
                        "graph": "CUDA graph per step, PDL between consecutive kernels",
                        "kernels_per_layer": round(launches_per_step / n_layers, 3),

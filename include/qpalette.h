@@ -193,6 +193,21 @@ qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype xt, int batc
  * QP_ERR_NCCL (incl. an asynchronous NCCL fault of an earlier call); QP_Y_ACCUMULATE is rejected. */
 qp_status qp_multi_fwd_sharded(qp_multi* m, const void* const* xs, qp_dtype xt, int batch, void* const* ys_full,
                                qp_dtype yt, void* comm, unsigned flags, void* stream);
+/* Row-sharded multi-layer forward with the all-gather FUSED into the engine epilogue (north star's
+ * all-gather step): every layer of m is this rank's row shard (qp_layer_shard; m_i =
+ * d_out_i rows); each final y value of this rank's rows is stored by the engine directly into every
+ * rank's y_full of that layer over peer-mapped memory (NVLink), at [b][rank * m_i + row] of the
+ * [batch][world * m_i] layout, so no collective kernel, gather scratch or permutation follows.
+ * ys_peers[i * world + k]: rank k's y_full of layer i (dtype yt, mapped with qp_ipc_open; this rank's
+ * own at k = rank); flag_peers[k]: rank k's flag array (unsigned[2 * world + 1], zeroed once), as in
+ * qp_linear_fwd_sharded_p2p, whose round-entry barrier and y_full reuse rule apply (a rank stores
+ * round n into a peer's y_full only after that peer entered round n); the call returns with a wait
+ * kernel enqueued that completes once every rank's rows of every layer have arrived. Every layer
+ * must have an engine variant (QP_ERR_UNSUPPORTED otherwise); QP_Y_ACCUMULATE / QP_INDEPENDENT are
+ * rejected (QP_ERR_INVALID_ARG). A peer that never arrives traps the wait kernel after 20 s. */
+qp_status qp_multi_fwd_sharded_p2p(qp_multi* m, const void* const* xs, qp_dtype xt, int batch,
+                                   void* const* ys_peers, unsigned* const* flag_peers, int rank, int world,
+                                   qp_dtype yt, unsigned flags, void* stream);
 /* n_layers; launch groups per qp_multi_fwd (n_launches: one engine launch each, or the per-layer
  * qp_linear_fwd path for a layer without an engine variant); how many are engine launches. */
 qp_status qp_multi_info(const qp_multi* m, int* n_layers, int* n_launches, int* n_engine_launches);

@@ -38,7 +38,7 @@ EXPORTS = [
     "qp_layer_free", "qp_last_error", "qp_version", "qp_shard_range", "qp_optimal_bits", "qp_plan_msq",
     "qp_linear_fwd_sharded_p2p", "qp_ipc_handle", "qp_ipc_open", "qp_ipc_close",
     "qp_codebook_set_scale", "qp_gather_permute", "qp_multi_create", "qp_multi_fwd", "qp_multi_info", "qp_multi_free",
-    "qp_multi_fwd_sharded", "qp_layer_shard_k", "qp_linear_fwd_ksharded",
+    "qp_multi_fwd_sharded", "qp_multi_fwd_sharded_p2p", "qp_layer_shard_k", "qp_linear_fwd_ksharded",
 ]
 
 
@@ -67,6 +67,7 @@ def lib() -> C.CDLL:
             "qp_multi_fwd": [vp, C.POINTER(vp), i, i, C.POINTER(vp), i, C.c_uint, vp],
             "qp_multi_info": [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i)],
             "qp_multi_fwd_sharded": [vp, C.POINTER(vp), i, i, C.POINTER(vp), i, vp, C.c_uint, vp],
+            "qp_multi_fwd_sharded_p2p": [vp, C.POINTER(vp), i, i, vp, vp, i, i, i, C.c_uint, vp],
             "qp_multi_free": [vp],
             "qp_rht_create": [u64, i, i, C.POINTER(vp)],
             "qp_rht_free": [vp],
@@ -446,6 +447,67 @@ class PeerGather:
     def forward(self, shard: "Layer", x, flags: int = 0, stream=None) -> None:
         check(lib().qp_linear_fwd_sharded_p2p(shard.h, _ptr(x), _dtype_code(x), self.batch, self._ys, self._fs,
                                               self.rank, self.world, _dtype_code(self.y), flags, _stream(stream)))
+
+    def close(self):
+        for p in self._opened:
+            lib().qp_ipc_close(C.c_void_p(p))
+        self._opened = []
+
+
+class MultiPeerGather:
+    """Fused all-gather destinations of a qp_multi over row shards (qp_multi_fwd_sharded_p2p): one
+    device buffer holds every layer's y_full [batch][world * m_i] (self.ys[i] are views), plus the
+    flag array; the two CUDA IPC handles are exchanged through torch.distributed (`group`, any
+    backend) and the peers' buffers mapped. world == 1 needs no process group."""
+
+    def __init__(self, world: int, rank: int, ms: list, batch: int, dtype=None, group=None):
+        import torch
+        dtype = dtype or torch.float32
+        self.world, self.rank, self.ms, self.batch = world, rank, list(ms), batch
+        eb = torch.empty(0, dtype=dtype).element_size()
+        # 256-byte aligned slices of one allocation
+        self._offs, off = [], 0
+        for m in self.ms:
+            self._offs.append(off)
+            off += (batch * world * m * eb + 255) // 256 * 256
+        self.buf = torch.zeros(off, dtype=torch.uint8, device="cuda")
+        self.ys = [self.buf[o:o + batch * world * m * eb].view(dtype).view(batch, world * m)
+                   for o, m in zip(self._offs, self.ms)]
+        self.flags = torch.zeros(2 * world + 1, dtype=torch.int32, device="cuda")
+        self._opened = []
+        if world == 1:
+            bases, fs = [self.buf.data_ptr()], [self.flags.data_ptr()]
+        else:
+            import torch.distributed as dist
+            hb, hf = (C.c_char * 72)(), (C.c_char * 72)()
+            check(lib().qp_ipc_handle(C.c_void_p(self.buf.data_ptr()), hb))
+            check(lib().qp_ipc_handle(C.c_void_p(self.flags.data_ptr()), hf))
+            allh = [None] * world
+            dist.all_gather_object(allh, (bytes(hb), bytes(hf)), group=group)
+            bases, fs = [], []
+            for k, (bb, bf) in enumerate(allh):
+                if k == rank:
+                    bases.append(self.buf.data_ptr())
+                    fs.append(self.flags.data_ptr())
+                    continue
+                pb, pf = C.c_void_p(), C.c_void_p()
+                check(lib().qp_ipc_open(bb, C.byref(pb)))
+                check(lib().qp_ipc_open(bf, C.byref(pf)))
+                self._opened += [pb.value, pf.value]
+                bases.append(pb.value)
+                fs.append(pf.value)
+            torch.cuda.synchronize()
+            dist.barrier(group=group)
+        n = len(self.ms)
+        self._ys = (C.c_void_p * (n * world))(*[bases[k] + self._offs[i] for i in range(n) for k in range(world)])
+        self._fs = (C.c_void_p * world)(*fs)
+
+    def forward(self, multi: "Multi", xs: list, flags: int = 0, stream=None) -> None:
+        assert len(xs) == len(self.ms) == multi.n_layers
+        xa = (C.c_void_p * len(xs))(*[_ptr(x) for x in xs])
+        check(lib().qp_multi_fwd_sharded_p2p(multi.h, xa, _dtype_code(xs[0]), self.batch, self._ys, self._fs,
+                                             self.rank, self.world, _dtype_code(self.ys[0]), flags,
+                                             _stream(stream)))
 
     def close(self):
         for p in self._opened:

@@ -338,19 +338,34 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   // needed, through an index the compiler cannot hoist (shfl of the layer index), so no per-layer
   // address set stays live across the decode.
   auto opaque = [&](int v) -> int { return __shfl_sync(0xffffffffu, v, 0); };
+  // a final y value: into y (fp32 / fp16, or y +=), or -- fused all-gather -- into every rank's y_full
+  auto store_final = [&](const EngOp& o, int bb, int row, float v) {
+    if (p.n_peers > 0) {
+      const size_t off = ((size_t)bb * p.n_peers + p.peer_rank) * o.d_out + row;
+#pragma unroll 1
+      for (int k = 0; k < p.n_peers; ++k) {
+        if (p.y_f32) reinterpret_cast<float*>(o.peer_y[k])[off] = v;
+        else reinterpret_cast<__half*>(o.peer_y[k])[off] = __float2half_rn(v);
+      }
+      return;
+    }
+    const size_t e = (size_t)bb * o.d_out + row;
+    if (p.y_f32) {
+      float* y = reinterpret_cast<float*>(o.y) + e;
+      *y = p.y_accum ? *y + v : v;
+    } else {
+      reinterpret_cast<__half*>(o.y)[e] = __float2half_rn(v);
+    }
+  };
   // wait until layer o_'s x' is complete in this launch (`ready` counts its finished rotation jobs
-  // and is reset by the last CTA out): relaxed polling, then one acquire
+  // and is reset by the last CTA out): acquire polling
   auto enter_op = [&](int o_) {
     const EngOp& o = p.op[o_];
     if (o.njobs > 0) {
+      // every poll is an acquire load: the load that sees the count complete is the acquire (one
+      // L2 round trip less than relaxed polling + a separate acquire)
       const unsigned want = (unsigned)o.njobs;
-      if (*reinterpret_cast<volatile const unsigned*>(o.ready) < want) {
-        for (;;) {
-          __nanosleep(32);
-          if (*reinterpret_cast<volatile const unsigned*>(o.ready) >= want) break;
-        }
-      }
-      (void)ld_acquire_u32(o.ready);
+      while (ld_acquire_u32(o.ready) < want) __nanosleep(32);
     }
   };
   float sc[RP][4];
@@ -447,22 +462,12 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       for (int h = 0; h < RP; ++h) {
         const uint32_t rth = RP * rt + h;                   // row tile
         if (seg_k0 == 0 && row_end) {                       // the whole row tile: store directly
-          void* yv = p.op[oe].y;
 #pragma unroll
           for (int m = 0; m < 2; ++m)
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-              if (bb < p.batch) {
-                const float v = acc[h][m][r] * sc[h][2 * m + (r >> 1)];
-                const size_t e = (size_t)bb * d_out + rth * kTileRows + row;
-                if (p.y_f32) {
-                  float* y = reinterpret_cast<float*>(yv) + e;
-                  *y = p.y_accum ? *y + v : v;
-                } else {
-                  reinterpret_cast<__half*>(yv)[e] = __float2half_rn(v);
-                }
-              }
+              if (bb < p.batch) store_final(p.op[oe], bb, rth * kTileRows + row, acc[h][m][r] * sc[h][2 * m + (r >> 1)]);
             }
         } else {
           float* wsb = p.op[oe].ws + rth * kTileRows;
@@ -482,19 +487,12 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
           if (done) {
             // every k tile of row tile rth is in the workspace: write y, re-zero the workspace
             __syncwarp();
-            void* yv = p.op[oe].y;
             for (int e = lane; e < kTileRows * p.batch; e += 32) {
               const int bb = e >> 5, row = e & 31;
               float* wp = wsb + (size_t)bb * d_out + row;
               const float v = __ldcg(wp);
               __stcg(wp, 0.f);
-              const size_t ye = (size_t)bb * d_out + rth * kTileRows + row;
-              if (p.y_f32) {
-                float* y = reinterpret_cast<float*>(yv) + ye;
-                *y = p.y_accum ? *y + v : v;
-              } else {
-                reinterpret_cast<__half*>(yv)[ye] = __float2half_rn(v);
-              }
+              store_final(p.op[oe], bb, rth * kTileRows + row, v);
             }
             if (lane == 0) st_relaxed(cnt, 0u);
           }
@@ -544,7 +542,14 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   // the last CTA out resets the launch's ready counters (every CTA is past its waits)
   __syncthreads();
   if (tid == 0) {
+    if (p.n_peers > 0) __threadfence_system();   // this CTA's peer stores before its arrival
     if (atom_add_acqrel(p.gen, 1u) == gridDim.x - 1) {
+      if (p.n_peers > 0) {
+        // every CTA's stores are in every y_full: deliver (fence / relaxed atomic / fence chain, as
+        // peer_signal; qp_peer_wait_kernel consumes one delivery per engine launch and rank)
+        __threadfence_system();
+        for (int k = 0; k < p.n_peers; ++k) atomicAdd_system(p.peer_flag[k] + p.peer_rank, 1u);
+      }
       for (int o_ = 0; o_ < p.n_ops; ++o_) st_relaxed(p.op[o_].ready, 0u);
       st_relaxed(p.gen, 0u);
       // this launch of the group has exited (QP_INDEPENDENT launches of the group wait for it)

@@ -1005,6 +1005,9 @@ cudaError_t launch_one(const GemvParams& prm, int grid, bool pdl, cudaStream_t s
 // with the atomic fp32 epilogue and a small decode table uses row-pair units (RP = 2) when d_out
 // has an even number of row tiles (QP_RP2_MIN_BATCH overrides the batch threshold; 9 disables).
 int env_no_xs();
+// the mbarrier area is 1024 B with its last word holding the in-order epilogue's generation: at most
+// 127 barriers (8 B each) over all warps, so QP_NS_MAX can never push barriers into the code ring
+constexpr int kBarStagesMax = 1016 / 8;
 int ns_cap();   // most code-ring stages per warp (QP_NS_MAX; the rest of shared memory is L1)
 int rp2_min_batch();
 int fused_rht_max_rounds();   // fused rotation: most rounds of in-CTA transforms worth doing
@@ -1042,7 +1045,7 @@ cudaError_t launch_plan(const GemvParams& prm0, int grid, bool pdl, cudaStream_t
   // table (VQ / NUQ / UNIF), whose ring keeps >= 2 stages of two tiles
   if (!DEQ && prm.y_atomic && !prm.y_ws && prm.batch >= rp2_min_batch() && prm.RT % 2 == 0 && PL::TAB <= 32768 &&
       PL::AVAIL >= PL::NWARP * 2 * 2 * PL::STAGE) {
-    prm.ns = (std::min)(ns_cap(), PL::AVAIL / (PL::NWARP * 2 * PL::STAGE));
+    prm.ns = (std::min)((std::min)(ns_cap(), kBarStagesMax / PL::NWARP), PL::AVAIL / (PL::NWARP * 2 * PL::STAGE));
     const int units = (prm.RT / 2) * prm.KT;
     if (grid > units) {
       grid = units;
@@ -1050,7 +1053,7 @@ cudaError_t launch_plan(const GemvParams& prm0, int grid, bool pdl, cudaStream_t
     }
     return launch_one<MODE, CLO, CHI, L, TB, REPS, false, 0, 2>(prm, grid, pdl, s);
   }
-  prm.ns = (std::min)(ns_cap(), PL::AVAIL / (PL::NWARP * PL::STAGE));
+  prm.ns = (std::min)((std::min)(ns_cap(), kBarStagesMax / PL::NWARP), PL::AVAIL / (PL::NWARP * PL::STAGE));
   return launch_one<MODE, CLO, CHI, L, TB, REPS, DEQ, 0>(prm, grid, pdl, s);
 }
 

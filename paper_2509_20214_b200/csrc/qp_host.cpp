@@ -999,7 +999,7 @@ extern "C" qp_status qp_linear_fwd_sharded_p2p(const qp_layer* shard, const void
   const qp_status st = qp_linear_fwd(shard, x, xt, batch, y_peers[rank], yt, flags | QP_DETERMINISTIC, stream);
   g_peer_out = nullptr;
   if (st != QP_OK) return st;
-  cudaError_t e = launch_peer_wait(flag_peers[rank], world, static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_peer_wait(flag_peers[rank], world, static_cast<cudaStream_t>(stream), 1);
   if (e != cudaSuccess) return cuda_fail(e, "peer wait kernel launch");
   return QP_OK;
 }
@@ -1120,7 +1120,7 @@ struct qp_multi {
   std::vector<__half*> d_xr;           // per layer: x' [8][d_in]
   std::vector<float*> d_ws;            // per layer: [8][d_out] fp32, zero between launches
   std::vector<int*> d_cnt;             // per layer: [RT] k-tile counters, zero between launches
-  unsigned* d_flags = nullptr;         // per layer: ready (+ 1 spare word)
+  unsigned* d_flags = nullptr;         // per layer: ready, kFlagStride words apart (own L2 slice)
   unsigned* d_gens = nullptr;          // per group [8]: exit counter, pad, 64-bit entry / exit counts
 };
 
@@ -1206,7 +1206,7 @@ extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_mu
     m->groups.push_back(gr);
     i = j;
   }
-  m->d_flags = static_cast<unsigned*>(dev_alloc((size_t)2 * n * 4));
+  m->d_flags = static_cast<unsigned*>(dev_alloc((size_t)kFlagStride * n * 4));
   m->d_gens = static_cast<unsigned*>(dev_alloc(m->groups.size() * 8 * 4));
   bool ok = m->d_flags && m->d_gens;
   for (int i = 0; i < n && ok; ++i) {
@@ -1219,7 +1219,7 @@ extern "C" qp_status qp_multi_create(const qp_layer* const* layers, int n, qp_mu
                cudaMemset(m->d_cnt.back(), 0, (size_t)(l->d_out / kTileRows) * 4) != cudaSuccess))
       ok = false;
   }
-  if (ok && (cudaMemset(m->d_flags, 0, (size_t)2 * n * 4) != cudaSuccess ||
+  if (ok && (cudaMemset(m->d_flags, 0, (size_t)kFlagStride * n * 4) != cudaSuccess ||
              cudaMemset(m->d_gens, 0, m->groups.size() * 8 * 4) != cudaSuccess))
     ok = false;
   // the memsets run on the legacy stream: complete them before any stream uses the object
@@ -1252,9 +1252,27 @@ extern "C" qp_status qp_multi_info(const qp_multi* m, int* n_layers, int* n_laun
   return QP_OK;
 }
 
+namespace {
+// fused all-gather destinations of qp_multi_fwd_sharded_p2p
+struct EngPeers {
+  int world, rank;
+  void* const* y;              // [n_layers * world]
+  unsigned* const* flag;       // [world]
+};
+
+qp_status multi_fwd_impl(qp_multi* m, const void* const* xs, qp_dtype xt, int batch, void* const* ys, qp_dtype yt,
+                         unsigned flags, void* stream, const EngPeers* peers);
+}  // namespace
+
 extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype xt, int batch, void* const* ys,
                                   qp_dtype yt, unsigned flags, void* stream) {
   if (!m || !xs || !ys) return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_multi_fwd");
+  return multi_fwd_impl(m, xs, xt, batch, ys, yt, flags, stream, nullptr);
+}
+
+namespace {
+qp_status multi_fwd_impl(qp_multi* m, const void* const* xs, qp_dtype xt, int batch, void* const* ys, qp_dtype yt,
+                         unsigned flags, void* stream, const EngPeers* peers) {
   const int n = (int)m->layers.size();
   for (int i = 0; i < n; ++i) {
     if (!ys[i]) return fail(QP_ERR_INVALID_ARG, "ys[%d] is NULL", i);
@@ -1272,6 +1290,10 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
   const bool pre = (flags & QP_X_PREROTATED) != 0;
   for (const auto& gr : m->groups) {
     if (!gr.launch) {
+      if (peers)
+        return fail(QP_ERR_UNSUPPORTED, "qp_multi_fwd_sharded_p2p: layer %d has no engine variant (the fused "
+                    "all-gather runs in the engine epilogue). Remedy: qp_linear_fwd_sharded_p2p per layer",
+                    gr.first);
       for (int i = gr.first; i < gr.first + gr.n; ++i) {
         qp_status st = qp_linear_fwd(m->layers[i], xs[i], xt, batch, ys[i], yt, layer_flags, stream);
         if (st != QP_OK) return st;
@@ -1329,10 +1351,17 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
       o.njobs = pre ? 0 : batch * (l->d_in / l->rht->block);
       jobs += o.njobs;
       if (o.njobs) scratch = std::max(scratch, l->rht->block * 4);
-      o.ready = m->d_flags + 2 * i;
+      o.ready = m->d_flags + (size_t)kFlagStride * i;
       o.y = ys[i];
       o.ws = m->d_ws[i];
       o.counters = m->d_cnt[i];
+      if (peers)
+        for (int k = 0; k < peers->world; ++k) o.peer_y[k] = peers->y[(size_t)i * peers->world + k];
+    }
+    if (peers) {
+      p.n_peers = peers->world;
+      p.peer_rank = peers->rank;
+      for (int k = 0; k < peers->world; ++k) p.peer_flag[k] = peers->flag[k];
     }
     p.total_jobs = jobs;
     p.rot_scratch_bytes = scratch;
@@ -1356,6 +1385,49 @@ extern "C" qp_status qp_multi_fwd(qp_multi* m, const void* const* xs, qp_dtype x
     if (e != cudaSuccess) return cuda_fail(e, "engine launch");
     count_launch();
   }
+  return QP_OK;
+}
+}  // namespace
+
+// Row-sharded multi-layer forward with the all-gather fused into the engine epilogue: every final y
+// value of this rank's rows is stored straight into every rank's y_full over NVLink (peer-mapped
+// pointers), the last CTA out of each engine launch delivers to every rank, and one wait kernel
+// consumes the deliveries -- no collective kernel, no gather scratch, no permutation (the stores
+// land in the [B][P m] layout). A round-entry barrier precedes the launch (the y_full reuse rule of
+// qp_linear_fwd_sharded_p2p).
+extern "C" qp_status qp_multi_fwd_sharded_p2p(qp_multi* m, const void* const* xs, qp_dtype xt, int batch,
+                                              void* const* ys_peers, unsigned* const* flag_peers, int rank,
+                                              int world, qp_dtype yt, unsigned flags, void* stream) {
+  if (!m || !xs || !ys_peers || !flag_peers)
+    return fail(QP_ERR_INVALID_ARG, "NULL argument to qp_multi_fwd_sharded_p2p");
+  if (world < 1 || world > kMaxGroup || rank < 0 || rank >= world)
+    return fail(QP_ERR_INVALID_ARG, "rank %d / world %d (1..%d ranks)", rank, world, kMaxGroup);
+  const int n = (int)m->layers.size();
+  for (int k = 0; k < world; ++k)
+    if (!flag_peers[k]) return fail(QP_ERR_INVALID_ARG, "flag_peers[%d] is NULL", k);
+  for (int i = 0; i < n * world; ++i)
+    if (!ys_peers[i]) return fail(QP_ERR_INVALID_ARG, "ys_peers[%d] is NULL", i);
+  if (flags & (QP_Y_ACCUMULATE | QP_INDEPENDENT))
+    return fail(QP_ERR_INVALID_ARG, "qp_multi_fwd_sharded_p2p: QP_Y_ACCUMULATE / QP_INDEPENDENT not supported (the "
+                "all-gather overwrites y_full; rounds are ordered by the entry barrier)");
+  int launches = 0;
+  for (const auto& gr : m->groups) {
+    if (!gr.launch)
+      return fail(QP_ERR_UNSUPPORTED, "qp_multi_fwd_sharded_p2p: layer %d has no engine variant. Remedy: "
+                  "qp_linear_fwd_sharded_p2p per layer", gr.first);
+    ++launches;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaError_t e = launch_peer_enter(flag_peers, rank, world, s); e != cudaSuccess)
+    return cuda_fail(e, "peer enter kernel launch");
+  const EngPeers pe{world, rank, ys_peers, flag_peers};
+  // ys: this rank's own y_full (argument checks only; the engine stores through pe)
+  std::vector<void*> own(n);
+  for (int i = 0; i < n; ++i) own[i] = ys_peers[(size_t)i * world + rank];
+  qp_status st = multi_fwd_impl(m, xs, xt, batch, own.data(), yt, flags, stream, &pe);
+  if (st != QP_OK) return st;
+  if (cudaError_t e = launch_peer_wait(flag_peers[rank], world, s, launches); e != cudaSuccess)
+    return cuda_fail(e, "peer wait kernel launch");
   return QP_OK;
 }
 

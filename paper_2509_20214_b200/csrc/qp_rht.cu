@@ -194,9 +194,9 @@ constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
 // Fused all-gather completion on this rank: flags_local[q] counts the launches rank q has
 // completed into our y_full; flags_local[world] is how many we have consumed. Waits until every
 // rank is one ahead, then consumes (graph-replay safe: no host-side epoch).
-__global__ void qp_peer_wait_kernel(unsigned* flags_local, int world) {
+__global__ void qp_peer_wait_kernel(unsigned* flags_local, int world, int n) {
   if (threadIdx.x != 0) return;
-  const unsigned want = flags_local[world] + 1u;
+  const unsigned want = flags_local[world] + (unsigned)n;   // n deliveries per rank this round
   const unsigned long long t0 = gtimer_ns();
   for (int q = 0; q < world; ++q) {
     unsigned v;
@@ -246,8 +246,8 @@ cudaError_t launch_peer_enter(unsigned* const* flag_peers, int rank, int world, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_peer_wait(unsigned* flags_local, int world, cudaStream_t s) {
-  qp_peer_wait_kernel<<<1, 32, 0, s>>>(flags_local, world);
+cudaError_t launch_peer_wait(unsigned* flags_local, int world, cudaStream_t s, int n) {
+  qp_peer_wait_kernel<<<1, 32, 0, s>>>(flags_local, world, n);
   count_launch();
   return cudaGetLastError();
 }

@@ -342,3 +342,25 @@ def test_activation_range_limit_r20():
     m.forward([torch.from_numpy(xo).cuda()], 1, [y3])
     torch.cuda.synchronize()
     assert not np.isfinite(y3.cpu().numpy()).all()
+
+
+@pytest.mark.parametrize("batch", [1, 5])
+def test_engine_p2p_world1_and_errors(batch):
+    """qp_multi_fwd_sharded_p2p at world size 1 (the stores go to this rank's own y_full; entry
+    barrier, delivery and wait kernel run) against the oracle, repeated; rejected flags / fallback."""
+    Lb = _lib()
+    items = _make(TB9_MIX[:4], first_id=300)
+    shards = [it[0].shard(0, 1) for it in items]
+    m = Lb.Multi(shards)
+    pg = Lb.MultiPeerGather(1, 0, [it[0].d_out for it in items], batch)
+    for rnd in range(3):
+        xs_np = [activations_fp16(batch, it[0].d_in, seed=400 + 10 * rnd + i) for i, it in enumerate(items)]
+        xs = [torch.from_numpy(x).cuda() for x in xs_np]
+        pg.forward(m, xs)
+        torch.cuda.synchronize()
+        for it, x, y in zip(items, xs_np, pg.ys):
+            assert np.max(linear.normwise_error(y.cpu().numpy(), _ref(it, x))) <= TOL
+    with pytest.raises(Lb.QPError):
+        pg.forward(m, xs, flags=Lb.QP_Y_ACCUMULATE)
+    with pytest.raises(Lb.QPError):
+        pg.forward(m, xs, flags=Lb.QP_INDEPENDENT)

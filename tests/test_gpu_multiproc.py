@@ -111,6 +111,93 @@ def test_p2p_allgather_across_processes(world):
     assert max(errs.values()) <= TOL, errs
 
 
+def _mworker(rank, world, port, specs, batch, ydt, results):
+    """The engine with the fused all-gather (qp_multi_fwd_sharded_p2p): this rank's row shards of
+    several layers in one qp_multi; every rank's y_full of every layer against the oracle."""
+    import torch.distributed as dist
+    from oracle import linear
+    from paper_2509_20214_b200 import _lib as L
+    from qp_synth import activations_fp16, channel_scales, random_code_bytes
+    from tests import qp_cases as Q
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full, codes, scales, shards = [], [], [], []
+        cbs = {}
+        for li, (d_out, d_in, scheme, x4) in enumerate(specs):
+            if (scheme, x4) not in cbs:
+                cbs[(scheme, x4)] = L.Codebook(scheme, x4, Q.load_fp16(scheme, x4), L=16)
+            c = random_code_bytes(Q.code_bytes(d_out, d_in, scheme, x4), 500 + li)
+            s = channel_scales(d_out, d_in)
+            f = L.Layer.from_codes(c, s, d_out, d_in, scheme, x4, cbs[(scheme, x4)], L.Rht(SEED, d_in))
+            full.append(f)
+            codes.append(c)
+            scales.append(s)
+            shards.append(f.shard(rank, world))
+        m = L.Multi(shards)
+        assert m.n_engine_launches == m.n_launches
+        dtype = torch.float32 if ydt == "f32" else torch.float16
+        pg = L.MultiPeerGather(world, rank, [d_out // world for d_out, _, _, _ in specs], batch, dtype=dtype)
+        st = torch.cuda.Stream()
+        errs = []
+
+        def check(xs_np):
+            for li, ((d_out, d_in, scheme, x4), x) in enumerate(zip(specs, xs_np)):
+                ref = linear.linear_from_codes(codes[li], d_out, d_in, scheme, x4, Q.oracle_codebook(scheme, x4),
+                                               scales[li], x.astype(np.float64), SEED)
+                errs.append(float(np.max(linear.normwise_error(pg.ys[li].float().cpu().numpy(), ref))))
+
+        for rnd in range(3):
+            xs_np = [activations_fp16(batch, sp[1], seed=700 + 10 * rnd + li) for li, sp in enumerate(specs)]
+            xs = [torch.from_numpy(x).cuda() for x in xs_np]
+            with torch.cuda.stream(st):
+                pg.forward(m, xs, stream=st)
+                st.synchronize()
+            check(xs_np)
+        xs = [torch.empty(batch, sp[1], dtype=torch.float16, device="cuda") for sp in specs]
+        with torch.cuda.stream(st):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                pg.forward(m, xs, stream=st)
+            for rep in range(3):
+                xs_np = [activations_fp16(batch, sp[1], seed=800 + 10 * rep + li) for li, sp in enumerate(specs)]
+                for x, xn in zip(xs, xs_np):
+                    x.copy_(torch.from_numpy(xn))
+                g.replay()
+                st.synchronize()
+                check(xs_np)
+        torch.cuda.synchronize()
+        dist.barrier()
+        results[rank] = max(errs)
+        pg.close()
+        del pg, m, shards, full
+        torch.cuda.synchronize()
+        dist.barrier()
+    except Exception as e:
+        results[-1 - rank] = repr(e)
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+MSPECS = [(512, 1024, "tcq", 10), (256, 1536, "half_tcq", 13), (1024, 512, "tcq", 16), (256, 14336, "tcq", 14)]
+
+
+@pytest.mark.parametrize("world,batch,ydt", [(2, 1, "f32"), (2, 8, "f16"), (4, 3, "f32"), (4, 1, "f16")])
+def test_engine_p2p_allgather_across_processes(world, batch, ydt):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_mworker, args=(world, _free_port(), MSPECS, batch, ydt, results), nprocs=world, join=True)
+    errs = dict(results)
+    assert sorted(errs) == list(range(world)), errs
+    assert max(errs.values()) <= TOL, errs
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("batch", [1, 3, 8])
 def test_gather_permute(world, batch):
