@@ -1153,6 +1153,22 @@ int eng_late_stages() {   // QP_ENG_LATE=1: fill ring stages 1.. only once x' is
   }
   return v;
 }
+double eng_row_cost() {   // QP_ENG_ROWCOST: per-row-tile overhead of a layer, in tiles (CTA range balance)
+  static double v = -1;
+  if (v < 0) {
+    const char* e = getenv("QP_ENG_ROWCOST");
+    v = e ? atof(e) : 0.0;
+  }
+  return v;
+}
+double eng_half_cost() {   // QP_ENG_HALFCOST: extra cost of a half-TCQ tile (two width runs per row)
+  static double v = -1;
+  if (v < 0) {
+    const char* e = getenv("QP_ENG_HALFCOST");
+    v = e ? atof(e) : 0.0;
+  }
+  return v;
+}
 double eng_job_tiles() {   // QP_ENG_JOB_TILES: tiles of GEMV work one rotation job displaces
   static double v = -1;
   if (v < 0) {
@@ -1368,17 +1384,31 @@ qp_status multi_fwd_impl(qp_multi* m, const void* const* xs, qp_dtype xt, int ba
     p.late_stages = eng_late_stages();
     p.independent = (flags & QP_INDEPENDENT) ? 1 : 0;
     const int grid = (int)std::min<long long>(std::min(num_sms(), kMaxEngCtas), tiles);
-    // CTA ranges over the flat tile order; the CTAs that run rotation jobs take job_tiles fewer
-    // tiles per job
+    // CTA ranges over the flat tile order, equal in estimated cost: a tile of layer l costs
+    // w_l = 1 + E / KT_l (a row tile's epilogue / activation switch, in tiles) + H [half-TCQ: two
+    // width runs per row tile]; the CTAs that run rotation jobs take job_tiles fewer tiles per job
     const uint32_t S = tiles;
     const double jt = eng_job_tiles() / rp;
-    const double base = ((double)S + jt * jobs) / grid;
+    double wl[kMaxEngOps], cum[kMaxEngOps + 1];
+    cum[0] = 0;
+    for (int k = 0; k < gr.n; ++k) {
+      const EngOp& o = p.op[k];
+      wl[k] = 1.0 + eng_row_cost() / o.KT + (o.c_lo != o.c_hi ? eng_half_cost() : 0.0);
+      cum[k + 1] = cum[k] + wl[k] * (double)((o.RT / rp) * o.KT);
+    }
+    auto tile_at = [&](double x) -> double {   // the flat unit index at cumulative cost x
+      int k = 0;
+      while (k + 1 < gr.n && x >= cum[k + 1]) ++k;
+      return p.op[k].tile0 + (x - cum[k]) / wl[k];
+    };
+    const double base = (cum[gr.n] + jt * jobs) / grid;
     double acc = 0;
     p.cta_begin[0] = 0;
     for (int c = 0; c < grid; ++c) {
       const int my_jobs = c < jobs ? (jobs - 1 - c) / grid + 1 : 0;
       acc += std::max(0.0, base - jt * my_jobs);
-      p.cta_begin[c + 1] = (uint32_t)std::min<double>(S, std::llround(acc));
+      p.cta_begin[c + 1] = (uint32_t)std::min<double>(S, std::llround(tile_at(std::min(acc, cum[gr.n]))));
+      if (p.cta_begin[c + 1] < p.cta_begin[c]) p.cta_begin[c + 1] = p.cta_begin[c];
     }
     p.cta_begin[grid] = S;
     cudaError_t e = gr.launch(p, grid, pdl, s);
