@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   // layer a warp's tiles are contiguous, row-tile-major), so the next copy starts there; the first
   // copy, a copy into a later layer and every RP = 2 copy compute the address.
   const uint8_t* f_ptr = nullptr;
+  const uint64_t pol = l2_evict_first_policy();   // once: a per-copy createpolicy costs ~6 issue slots a tile
   auto fetch_ahead = [&](int st, uint32_t dep, uint32_t d, uint32_t h_, bool cont, int oi_, uint32_t rt_, uint32_t kt_,
                          uint32_t left_, uint32_t opk_) {
     const uint8_t* src;
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     if (elect_one()) {
       const uint32_t bar = bars + 8u * st;
       mbar_expect_tx(bar, nb);
-      bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, src, nb, bar, l2_evict_first_policy());
+      bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, src, nb, bar, pol);
     }
     f_ptr = src + nb;
   };

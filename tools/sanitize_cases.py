@@ -69,6 +69,13 @@ def main():
         m.forward(xs, batch, ys)
         m.forward(xs, batch, ys, flags=QL.QP_Y_ACCUMULATE)
         m.forward(xs, batch, [y.half() for y in ys])
+    # the engine with the fused all-gather epilogue at world size 1 (peer stores, delivery, entry
+    # barrier, wait kernel) over row shards of the tb = 9 layers
+    shards = [e[0].shard(0, 1) for e in eng[:3]]
+    m2 = QL.Multi(shards)
+    pg = QL.MultiPeerGather(1, 0, [o_ for (_, _, o_, _) in specs[:3]], 2)
+    for _ in range(2):
+        pg.forward(m2, [torch.from_numpy(activations_fp16(2, i_)).cuda() for (_, _, _, i_) in specs[:3]])
     # GPU trellis encoder
     W = gaussian_weights(32, 256, seed=0).astype(np.float32)
     QL.Layer.quantize_offline(W, "tcq", 10, QL.Codebook("tcq", 10, P.load_fp16("tcq", 10), L=16), QL.Rht(7, 256),
