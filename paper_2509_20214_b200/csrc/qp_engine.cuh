@@ -217,8 +217,10 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   }
 
   // ---- the code ring (one tile per stage; the tile sequence is unit-major, h = 0..RP-1 inside) --
-  const uint32_t ring = smem_u32(smem + PL::RING_OFF) + (uint32_t)(warp * NS * PL::STAGE);
-  const uint32_t bars = smem_u32(smem + PL::BAR_OFF) + (uint32_t)(warp * NS * 8);
+  // (from the constant dynamic-shared-memory base checked above: rematerialising these from the
+  // generic pointer cost an S2R SR_CgaCtaId + LEA in every tile of the loop)
+  const uint32_t ring = kDynSmemBase + PL::RING_OFF + (uint32_t)(warp * NS * PL::STAGE);
+  const uint32_t bars = kDynSmemBase + PL::BAR_OFF + (uint32_t)(warp * NS * 8);
   // Copy tile h_ of the unit d units after the decode cursor (oi_, rt_, kt_, left_, opk_) into stage
   // st (an elected lane issues). RP = 1: f_ptr is the address following the previous copy (inside a
   // layer a warp's tiles are contiguous, row-tile-major), so the next copy starts there; the first
@@ -366,7 +368,17 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       // every poll is an acquire load: the load that sees the count complete is the acquire (one
       // L2 round trip less than relaxed polling + a separate acquire)
       const unsigned want = (unsigned)o.njobs;
+#ifdef QP_ENG_RELAXED_POLL
+      if (*reinterpret_cast<volatile const unsigned*>(o.ready) < want) {
+        for (;;) {
+          __nanosleep(32);
+          if (*reinterpret_cast<volatile const unsigned*>(o.ready) >= want) break;
+        }
+      }
+      (void)ld_acquire_u32(o.ready);
+#else
       while (ld_acquire_u32(o.ready) < want) __nanosleep(32);
+#endif
     }
   };
   float sc[RP][4];
@@ -437,10 +449,26 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
             const uint4 v = lds128(src + w * 512);
             cur[4 * w] = v.x; cur[4 * w + 1] = v.y; cur[4 * w + 2] = v.z; cur[4 * w + 3] = v.w;
           }
-          // the stage is free once every lane's shared loads have returned (see qp_gemv_kernel)
-          const uint32_t dep = __reduce_or_sync(0xffffffffu, cur[4 * C - 1] & p.zero);
+          // the stage is free once every lane's shared loads have returned: the warp reduction
+          // depends on one word of EVERY load (ptxas reorders the independent LDS.128s, so the last
+          // one in program order is not the last issued: depending on it alone let the refill
+          // overwrite words still in flight -- a race the shorter fast-path issue exposed)
+          uint32_t any = 0;
+#pragma unroll
+          for (int w = 0; w < C; ++w) any |= cur[4 * w + 3];
+          const uint32_t dep = __reduce_or_sync(0xffffffffu, any & p.zero);
           const uint32_t pos = (tt - a) * RP + h + NS;         // the tile sequence position to fetch
-          if (pos < ntiles) fetch_ahead(st, dep, (h + NS) / RP, (h + NS) % RP, true, oi, rt, kt, left, opk);
+          if (RP == 1 && i + (uint32_t)NS < n) {
+            // the tile NS ahead is in this run: same width C, right after the previous copy
+            if (elect_one()) {
+              const uint32_t bar = bars + 8u * st;
+              mbar_expect_tx(bar, 512u * C);
+              bulk_g2s(ring + (uint32_t)(st * PL::STAGE) + dep, f_ptr, 512u * C, bar, pol);
+            }
+            f_ptr += 512u * C;
+          } else if (pos < ntiles) {
+            fetch_ahead(st, dep, (h + NS) / RP, (h + NS) % RP, true, oi, rt, kt, left, opk);
+          }
           const __half* x_hi = (xrow && h == 0) ? xl + kt * kTileCols + 32 : nullptr;
           const __half* x_next = h == RP - 1 ? x_nx : nullptr;
           tile_body<MODE, C, L, TB, REPS, false, false, true>(cur, laneoff, mulk, xb, acc[h], nullptr, 0, x_hi, x_next,

@@ -730,10 +730,14 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
       }
       if (h == RP - 1) {
         // The stage is free once every lane's shared loads have returned: a warp reduction over
-        // the last loaded word of each lane (in-order shared pipeline: the earlier loads are done
-        // too) makes lane 0's refill depend on all of them (p.zero == 0 keeps the value unchanged).
-        const uint32_t last = (CLO == CHI || c == CMAX) ? cur[4 * CMAX - 1] : cur[4 * CLO - 1];
-        const uint32_t dep = __reduce_or_sync(0xffffffffu, last & p.zero);
+        // one word of EVERY load of each lane makes lane 0's refill depend on all of them (p.zero
+        // == 0 keeps the value unchanged). (ptxas reorders the independent LDS.128s, so the last
+        // load in program order need not be the last one issued.)
+        uint32_t any = 0;
+#pragma unroll
+        for (int i = 0; i < CMAX; ++i)
+          if (CLO == CHI || i < c) any |= cur[4 * i + 3];
+        const uint32_t dep = __reduce_or_sync(0xffffffffu, any & p.zero);
         if (lane == 0 && t + NS < b) fetch(f_ptr, tile_bytes(kt_f), st, dep);
 #ifdef QP_L2_PREFETCH
         // warm L2 with the unit after the one just requested (its bulk copy then hits L2)
