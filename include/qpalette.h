@@ -199,7 +199,8 @@ qp_status qp_multi_fwd_sharded(qp_multi* m, const void* const* xs, qp_dtype xt, 
  * rank's y_full of that layer over peer-mapped memory (NVLink), at [b][rank * m_i + row] of the
  * [batch][world * m_i] layout, so no collective kernel, gather scratch or permutation follows.
  * ys_peers[i * world + k]: rank k's y_full of layer i (dtype yt, mapped with qp_ipc_open; this rank's
- * own at k = rank); flag_peers[k]: rank k's flag array (unsigned[2 * world + 1], zeroed once), as in
+ * own at k = rank), laid out identically on every rank: layer i's buffer at the same byte offset from
+ * layer 0's on every rank (QP_ERR_INVALID_ARG otherwise); flag_peers[k]: rank k's flag array (unsigned[2 * world + 1], zeroed once), as in
  * qp_linear_fwd_sharded_p2p, whose round-entry barrier and y_full reuse rule apply (a rank stores
  * round n into a peer's y_full only after that peer entered round n); the call returns with a wait
  * kernel enqueued that completes once every rank's rows of every layer have arrived. Every layer

@@ -169,6 +169,30 @@ __device__ unsigned long long g_eng_wl[kMaxEngCtas][16];   // per-warp main-loop
 #define QP_TL(k) do { } while (0)
 #endif
 
+// Fused all-gather store (qp_multi_fwd_sharded_p2p): the final value of (batch row bb, row) of layer o
+// into every rank's y_full. Out of line: the epilogues sit inside the decode loop, whose code must stay
+// small (inlined here it grew the TCQ tb = 10 kernel by ~20 % and slowed it 18 %: instruction cache).
+__device__ __noinline__ void store_peers(const EngParams& p, const EngOp& o, int bb, int row, float v) {
+  const size_t eb = p.y_f32 ? 4 : 2;
+  const size_t off = (size_t)(reinterpret_cast<const char*>(o.y) - p.peer_base[p.peer_rank]) +
+                     (((size_t)bb * p.n_peers + p.peer_rank) * o.d_out + row) * eb;
+#pragma unroll 1
+  for (int k = 0; k < p.n_peers; ++k) {
+    if (p.y_f32) *reinterpret_cast<float*>(p.peer_base[k] + off) = v;
+    else *reinterpret_cast<__half*>(p.peer_base[k] + off) = __float2half_rn(v);
+  }
+}
+
+// The fused all-gather's launch-exit protocol, out of line (system-scope fences inside the kernel body
+// change how ptxas lowers the workspace reductions): arrive = this CTA's peer stores fenced before its
+// arrival on the exit counter; deliver = the last CTA bumps this rank's delivery counter on every rank.
+__device__ __noinline__ void peer_fence() { __threadfence_system(); }
+__device__ __noinline__ void peer_deliver(const EngParams& p) {
+  __threadfence_system();
+#pragma unroll 1
+  for (int k = 0; k < p.n_peers; ++k) atomicAdd_system(p.peer_flag[k] + p.peer_rank, 1u);
+}
+
 // RP: row tiles per work unit. RP = 2 (batch >= 4): a unit is the two row tiles of a row pair at one
 // k tile, decoded back to back with the same activation fragments -- half the x' loads, which are
 // the batch-8 bottleneck (MIO: 4 KB of x' per 32x256 tile at batch 8).
@@ -341,25 +365,6 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   // needed, through an index the compiler cannot hoist (shfl of the layer index), so no per-layer
   // address set stays live across the decode.
   auto opaque = [&](int v) -> int { return __shfl_sync(0xffffffffu, v, 0); };
-  // a final y value: into y (fp32 / fp16, or y +=), or -- fused all-gather -- into every rank's y_full
-  auto store_final = [&](const EngOp& o, int bb, int row, float v) {
-    if (p.n_peers > 0) {
-      const size_t off = ((size_t)bb * p.n_peers + p.peer_rank) * o.d_out + row;
-#pragma unroll 1
-      for (int k = 0; k < p.n_peers; ++k) {
-        if (p.y_f32) reinterpret_cast<float*>(o.peer_y[k])[off] = v;
-        else reinterpret_cast<__half*>(o.peer_y[k])[off] = __float2half_rn(v);
-      }
-      return;
-    }
-    const size_t e = (size_t)bb * o.d_out + row;
-    if (p.y_f32) {
-      float* y = reinterpret_cast<float*>(o.y) + e;
-      *y = p.y_accum ? *y + v : v;
-    } else {
-      reinterpret_cast<__half*>(o.y)[e] = __float2half_rn(v);
-    }
-  };
   // wait until layer o_'s x' is complete in this launch (`ready` counts its finished rotation jobs
   // and is reset by the last CTA out): acquire polling
   auto enter_op = [&](int o_) {
@@ -458,7 +463,11 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
           for (int w = 0; w < C; ++w) any |= cur[4 * w + 3];
           const uint32_t dep = __reduce_or_sync(0xffffffffu, any & p.zero);
           const uint32_t pos = (tt - a) * RP + h + NS;         // the tile sequence position to fetch
+#ifdef QP_ENG_NO_FASTPATH
+          if (false) {
+#else
           if (RP == 1 && i + (uint32_t)NS < n) {
+#endif
             // the tile NS ahead is in this run: same width C, right after the previous copy
             if (elect_one()) {
               const uint32_t bar = bars + 8u * st;
@@ -491,12 +500,26 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
       for (int h = 0; h < RP; ++h) {
         const uint32_t rth = RP * rt + h;                   // row tile
         if (seg_k0 == 0 && row_end) {                       // the whole row tile: store directly
+          void* yv = p.op[oe].y;
 #pragma unroll
           for (int m = 0; m < 2; ++m)
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-              if (bb < p.batch) store_final(p.op[oe], bb, rth * kTileRows + row, acc[h][m][r] * sc[h][2 * m + (r >> 1)]);
+              if (bb < p.batch) {
+                const float v = acc[h][m][r] * sc[h][2 * m + (r >> 1)];
+                if (p.n_peers > 0) {
+                  store_peers(p, p.op[oe], bb, rth * kTileRows + row, v);
+                } else {
+                  const size_t e = (size_t)bb * d_out + rth * kTileRows + row;
+                  if (p.y_f32) {
+                    float* y = reinterpret_cast<float*>(yv) + e;
+                    *y = p.y_accum ? *y + v : v;
+                  } else {
+                    reinterpret_cast<__half*>(yv)[e] = __float2half_rn(v);
+                  }
+                }
+              }
             }
         } else {
           float* wsb = p.op[oe].ws + rth * kTileRows;
@@ -505,7 +528,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
-              if (bb < p.batch) atomicAdd(wsb + (size_t)bb * d_out + row, acc[h][m][r] * sc[h][2 * m + (r >> 1)]);
+              if (bb < p.batch) red_add_f32(wsb + (size_t)bb * d_out + row, acc[h][m][r] * sc[h][2 * m + (r >> 1)]);
             }
           const int nk = (int)kt - seg_k0 + 1;
           unsigned* cnt = reinterpret_cast<unsigned*>(p.op[oe].counters + rth);
@@ -516,12 +539,21 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
           if (done) {
             // every k tile of row tile rth is in the workspace: write y, re-zero the workspace
             __syncwarp();
+            void* yv = p.op[oe].y;
             for (int e = lane; e < kTileRows * p.batch; e += 32) {
               const int bb = e >> 5, row = e & 31;
               float* wp = wsb + (size_t)bb * d_out + row;
               const float v = __ldcg(wp);
               __stcg(wp, 0.f);
-              store_final(p.op[oe], bb, rth * kTileRows + row, v);
+              const size_t ye = (size_t)bb * d_out + rth * kTileRows + row;
+              if (p.n_peers > 0) {
+                store_peers(p, p.op[oe], bb, rth * kTileRows + row, v);
+              } else if (p.y_f32) {
+                float* y = reinterpret_cast<float*>(yv) + ye;
+                *y = p.y_accum ? *y + v : v;
+              } else {
+                reinterpret_cast<__half*>(yv)[ye] = __float2half_rn(v);
+              }
             }
             if (lane == 0) st_relaxed(cnt, 0u);
           }
@@ -571,14 +603,11 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   // the last CTA out resets the launch's ready counters (every CTA is past its waits)
   __syncthreads();
   if (tid == 0) {
-    if (p.n_peers > 0) __threadfence_system();   // this CTA's peer stores before its arrival
+    if (p.n_peers > 0) peer_fence();             // this CTA's peer stores before its arrival
     if (atom_add_acqrel(p.gen, 1u) == gridDim.x - 1) {
-      if (p.n_peers > 0) {
-        // every CTA's stores are in every y_full: deliver (fence / relaxed atomic / fence chain, as
-        // peer_signal; qp_peer_wait_kernel consumes one delivery per engine launch and rank)
-        __threadfence_system();
-        for (int k = 0; k < p.n_peers; ++k) atomicAdd_system(p.peer_flag[k] + p.peer_rank, 1u);
-      }
+      // every CTA's stores are in every y_full: deliver (fence / relaxed atomic / fence chain, as
+      // peer_signal; qp_peer_wait_kernel consumes one delivery per engine launch and rank)
+      if (p.n_peers > 0) peer_deliver(p);
       for (int o_ = 0; o_ < p.n_ops; ++o_) st_relaxed(p.op[o_].ready, 0u);
       st_relaxed(p.gen, 0u);
       // this launch of the group has exited (QP_INDEPENDENT launches of the group wait for it)

@@ -123,6 +123,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
       :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
 }
+// fire-and-forget fp32 add (RED, no return): atomicAdd with an unused result is not always lowered to
+// RED -- in kernels that also contain system-scope fences ptxas keeps a returning ATOM. No "memory"
+// clobber: the reductions are relaxed (ordered before the completion counter's acq_rel atomic, itself
+// a volatile asm) and must not pin the surrounding loads / stores of the epilogue.
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" :: "l"(p), "f"(v));
+}
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
@@ -813,7 +820,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
               for (int r = 0; r < 4; ++r) {
                 const int row = 16 * m + g + 8 * (r >> 1), bb = 2 * q + (r & 1);
                 if (bb < p.batch)
-                  atomicAdd(yb + (size_t)bb * p.ldy[i] + row, acc[2 * h + m][r] * sc[4 * h + 2 * m + (r >> 1)]);
+                  red_add_f32(yb + (size_t)bb * p.ldy[i] + row, acc[2 * h + m][r] * sc[4 * h + 2 * m + (r >> 1)]);
               }
             if (RP == 1 && p.y_ws) {
               // count the k tiles this warp contributed; the warp that completes the row tile's KT
@@ -929,7 +936,7 @@ __global__ void __launch_bounds__(Plan<MODE, CLO, CHI, TB, REPS, (XM != 0)>::NWA
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int row = (lane + 32 * k) >> 3;
-          atomicAdd(yb + row, v[k] * scale_of(rt, row));     // compiles to RED.ADD.F32
+          red_add_f32(yb + row, v[k] * scale_of(rt, row));
         }
       }
       continue;

@@ -1371,13 +1371,14 @@ qp_status multi_fwd_impl(qp_multi* m, const void* const* xs, qp_dtype xt, int ba
       o.y = ys[i];
       o.ws = m->d_ws[i];
       o.counters = m->d_cnt[i];
-      if (peers)
-        for (int k = 0; k < peers->world; ++k) o.peer_y[k] = peers->y[(size_t)i * peers->world + k];
     }
     if (peers) {
       p.n_peers = peers->world;
       p.peer_rank = peers->rank;
-      for (int k = 0; k < peers->world; ++k) p.peer_flag[k] = peers->flag[k];
+      for (int k = 0; k < peers->world; ++k) {
+        p.peer_base[k] = static_cast<char*>(peers->y[k]);   // layer 0's y_full on rank k
+        p.peer_flag[k] = peers->flag[k];
+      }
     }
     p.total_jobs = jobs;
     p.rot_scratch_bytes = scratch;
@@ -1437,6 +1438,17 @@ extern "C" qp_status qp_multi_fwd_sharded_p2p(qp_multi* m, const void* const* xs
     if (!flag_peers[k]) return fail(QP_ERR_INVALID_ARG, "flag_peers[%d] is NULL", k);
   for (int i = 0; i < n * world; ++i)
     if (!ys_peers[i]) return fail(QP_ERR_INVALID_ARG, "ys_peers[%d] is NULL", i);
+  // every rank's y_full buffers must sit at the same offsets from that rank's layer-0 buffer (the
+  // kernel addresses rank k's copy as base_k + offset)
+  for (int i = 1; i < n; ++i) {
+    const std::ptrdiff_t off = static_cast<const char*>(ys_peers[(size_t)i * world + rank]) -
+                               static_cast<const char*>(ys_peers[rank]);
+    for (int k = 0; k < world; ++k)
+      if (static_cast<const char*>(ys_peers[(size_t)i * world + k]) - static_cast<const char*>(ys_peers[k]) != off)
+        return fail(QP_ERR_INVALID_ARG, "qp_multi_fwd_sharded_p2p: layer %d's y_full on rank %d is not at the same "
+                    "offset from layer 0's as on this rank. Remedy: carve every rank's y_full buffers out of one "
+                    "allocation in the same order (MultiPeerGather does)", i, k);
+  }
   if (flags & (QP_Y_ACCUMULATE | QP_INDEPENDENT))
     return fail(QP_ERR_INVALID_ARG, "qp_multi_fwd_sharded_p2p: QP_Y_ACCUMULATE / QP_INDEPENDENT not supported (the "
                 "all-gather overwrites y_full; rounds are ordered by the entry barrier)");

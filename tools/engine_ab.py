@@ -32,6 +32,11 @@ SETS = {
     "one_big": [(14336, 4096, "tcq", 10)],
     "one_down": [(4096, 14336, "tcq", 10)],
     "one_vq": [(4096, 4096, "vq", 12)],
+    # the four launches of the C5 decoder layer (tools/decoder_layer.py --engine)
+    "c5_qkv": [(4096, 4096, "half_tcq", 17), (1024, 4096, "half_tcq", 17), (1024, 4096, "half_tcq", 17)],
+    "c5_o": [(4096, 4096, "nuq", 16)],
+    "c5_gu": [(14336, 4096, "tcq", 12), (14336, 4096, "tcq", 12)],
+    "c5_down": [(4096, 14336, "vq", 12)],
 }
 
 
