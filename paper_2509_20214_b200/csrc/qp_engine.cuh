@@ -170,9 +170,9 @@ __device__ unsigned long long g_eng_wl[kMaxEngCtas][16];   // per-warp main-loop
 #endif
 
 // Fused all-gather store (qp_multi_fwd_sharded_p2p): the final value of (batch row bb, row) of layer o
-// into every rank's y_full. Out of line: the epilogues sit inside the decode loop, whose code must stay
-// small (inlined here it grew the TCQ tb = 10 kernel by ~20 % and slowed it 18 %: instruction cache).
-__device__ __noinline__ void store_peers(const EngParams& p, const EngOp& o, int bb, int row, float v) {
+// into every rank's y_full. (Inline on purpose: as __noinline__ calls these helpers made every engine
+// variant 1-6 % slower -- call-site register constraints; profiles/r2/v5/peer_helpers_ab.txt.)
+__device__ __forceinline__ void store_peers(const EngParams& p, const EngOp& o, int bb, int row, float v) {
   const size_t eb = p.y_f32 ? 4 : 2;
   const size_t off = (size_t)(reinterpret_cast<const char*>(o.y) - p.peer_base[p.peer_rank]) +
                      (((size_t)bb * p.n_peers + p.peer_rank) * o.d_out + row) * eb;
@@ -183,11 +183,10 @@ __device__ __noinline__ void store_peers(const EngParams& p, const EngOp& o, int
   }
 }
 
-// The fused all-gather's launch-exit protocol, out of line (system-scope fences inside the kernel body
-// change how ptxas lowers the workspace reductions): arrive = this CTA's peer stores fenced before its
-// arrival on the exit counter; deliver = the last CTA bumps this rank's delivery counter on every rank.
-__device__ __noinline__ void peer_fence() { __threadfence_system(); }
-__device__ __noinline__ void peer_deliver(const EngParams& p) {
+// The fused all-gather's launch-exit protocol: arrive = this CTA's peer stores fenced before its arrival
+// on the exit counter; deliver = the last CTA bumps this rank's delivery counter on every rank.
+__device__ __forceinline__ void peer_fence() { __threadfence_system(); }
+__device__ __forceinline__ void peer_deliver(const EngParams& p) {
   __threadfence_system();
 #pragma unroll 1
   for (int k = 0; k < p.n_peers; ++k) atomicAdd_system(p.peer_flag[k] + p.peer_rank, 1u);

@@ -5,7 +5,7 @@ import sys
 cur, res = None, {}
 for line in open(sys.argv[1]):
     line = line.strip()
-    if line.split(" ")[0] in ("old", "new", "base", "mulhi", "v3", "cur", "head", "cur_rp", "np", "rp"):
+    if line.split(" ")[0] in ("old", "new", "base", "mulhi", "v3", "cur", "head", "cur_rp", "np", "rp", "va", "vb"):
         cur = line
     elif line.startswith("{"):
         d = json.loads(line)
