@@ -67,6 +67,9 @@ struct EPlan {
   static constexpr int RING_OFF = TAB + 1024;
   static constexpr int AVAIL = SMEM_MAX - RING_OFF;
   static_assert(AVAIL >= NWARP * STAGE, "engine shared-memory plan does not fit");
+  // ring stages per warp, a compile-time constant (the ring index arithmetic of every tile folds):
+  // 2 where they fit (the rest of shared memory is L1 for the activations), else 1
+  static constexpr int NS = AVAIL / (NWARP * STAGE) >= 2 ? 2 : 1;
   static_assert(MODE != DEC_LUT2 || CMIN == CMAX, "LUT2 tables depend on c: one width per engine variant");
 };
 
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     qp_engine_kernel(const __grid_constant__ EngParams p) {
   using PL = EPlan<MODE, L, TB, REPS, CMIN, CMAX>;
   constexpr int NWARP = PL::NWARP;
-  const int NS = p.ns;
+  constexpr int NS = PL::NS;
   uint8_t* smem = qp_smem;
   if (threadIdx.x == 0 && smem_u32(qp_smem) != kDynSmemBase) __trap();
   // warp index through a lane-0 broadcast: provably warp-uniform to the compiler, so the ring /
@@ -621,7 +624,7 @@ struct EngineVariant {
   static cudaError_t launch(const EngParams& prm0, int grid, bool pdl, cudaStream_t s) {
     using PL = EPlan<MODE, L, TB, REPS, CMIN, CMAX>;
     EngParams prm = prm0;
-    prm.ns = (std::min)((std::min)(ns_cap(), 1024 / (PL::NWARP * 8)), PL::AVAIL / (PL::NWARP * PL::STAGE));
+    prm.ns = PL::NS;   // (QP_NS_MAX applies to the per-layer kernel only)
     int smem = PL::RING_OFF + PL::NWARP * prm.ns * PL::STAGE;
     smem = (std::max)(smem, prm.rot_scratch_bytes);
     if (smem > PL::SMEM_MAX) return cudaErrorInvalidValue;
