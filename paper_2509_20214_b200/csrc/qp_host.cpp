@@ -1169,13 +1169,16 @@ double eng_half_cost() {   // QP_ENG_HALFCOST: extra cost of a half-TCQ tile (tw
   }
   return v;
 }
-double eng_job_tiles() {   // QP_ENG_JOB_TILES: tiles of GEMV work one rotation job displaces
-  static double v = -1;
-  if (v < 0) {
+double eng_job_tiles(int batch) {   // QP_ENG_JOB_TILES: tiles of GEMV work one rotation job displaces
+  // A job (one Hadamard block of one batch row) costs about as much as 16 tiles at batch 1; a tile's
+  // cost grows with the batch (8 activation rows per MMA, x' loads), so fewer tiles per job above it:
+  // 16 * 8 / (7 + batch) = 16 at batch 1, 8.5 at batch 8 (A/B: batch 8 -2 to -6 %, profiles/r2/v5/job_tiles_ab.txt)
+  static double v = -2;
+  if (v == -2) {
     const char* e = getenv("QP_ENG_JOB_TILES");
-    v = e ? atof(e) : 16.0;
+    v = e ? atof(e) : -1.0;
   }
-  return v;
+  return v >= 0 ? v : 16.0 * 8.0 / (7.0 + batch);
 }
 void multi_release(qp_multi* m) {
   for (auto p : m->d_xr) dev_free(p);
@@ -1389,7 +1392,7 @@ qp_status multi_fwd_impl(qp_multi* m, const void* const* xs, qp_dtype xt, int ba
     // w_l = 1 + E / KT_l (a row tile's epilogue / activation switch, in tiles) + H [half-TCQ: two
     // width runs per row tile]; the CTAs that run rotation jobs take job_tiles fewer tiles per job
     const uint32_t S = tiles;
-    const double jt = eng_job_tiles() / rp;
+    const double jt = eng_job_tiles(batch) / rp;
     double wl[kMaxEngOps], cum[kMaxEngOps + 1];
     cum[0] = 0;
     for (int k = 0; k < gr.n; ++k) {
