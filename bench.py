@@ -620,8 +620,8 @@ def main():
             batch_lines[f"b{b_}"]["traffic"] = round(tr) if tr else None
 
     # ---- end to end through the public API with host buffers (N=1 only) ------------------
-    # Every step: one H2D copy of the step's 9 activation vectors from pinned host memory, the 9
-    # qp_linear_fwd calls, one D2H copy of the 9 results into pinned host memory -- captured with
+    # Every step: one H2D copy of the step's 9 activation vectors from pinned host memory, the step's
+    # forward (one qp_multi_fwd), one D2H copy of the 9 results into pinned host memory -- captured with
     # the forwards in a CUDA graph per replica (as a serving loop would), timed with events.
     e2e = None
     if world == 1:
@@ -712,17 +712,18 @@ def main():
         assert all(torch.isfinite(t).all() for t in hys), "non-finite y read back"
         e2e = {"value": round(step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4),
-               "method": "per step: 1 H2D copy of all activations from pinned host memory (copy stream), the 9 "
-                         "qp_linear_fwd calls (CUDA graph), 1 D2H copy of all outputs into pinned host memory "
+               "method": "per step: 1 H2D copy of all activations from pinned host memory (copy stream), the "
+                         "step's forward (qp_multi_fwd: one engine launch; CUDA graph), 1 D2H copy of all outputs "
+                         "into pinned host memory "
                          "(second copy stream); copies of neighbouring steps overlap the forwards; events",
                "serial_value": round(step_bytes / (e2e_ms_serial * 1e-3) / 1e9, 2),
                "serial_ms_per_step": round(e2e_ms_serial, 4)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nb, dt = oracle_sample(layers, budget_rows=512)
+        nb, dt = oracle_sample(layers, budget_rows=1536)
         cpu = {"value": round(nb / dt / 1e9, 6), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": "first 512 rows of each of the 9 C2 layers: float64 decode + RHT + matvec (batch 1)",
+               "sample": "first 1536 rows of each of the 9 C2 layers: float64 decode + RHT + matvec (batch 1)",
                "seconds": round(dt, 2), **cpu_info()}
 
     if rank == 0:
@@ -736,7 +737,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f16", "data": "synthetic",
             "config": {"workload": "C2: Llama-3.1-8B (4096x4096, 14336x4096, 4096x14336) x TCQ-2.5 / half-TCQ-3.25 / "
-                                   "TCQ-4.0 (L=16), rotation + fused dequant-GEMV per layer (qp_linear_fwd on raw x)",
+                                   "TCQ-4.0 (L=16), rotation + fused dequant-GEMV per layer on raw fp16 x",
                        "batch": batch, "layers_per_step": n_layers, "us_per_layer": round(ms * 1e3 / n_layers, 3),
                        "parallelism": ((f"row-shard x{world}: engine over each rank's shards with the all-gather "
                                         f"fused into its epilogue (peer stores over NVLink)" if allgather == "p2p" else
