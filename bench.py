@@ -298,8 +298,13 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    # the row-sharded (N > 1) path; QP_BENCH_FORCE_SHARDED=1 runs it at N = 1 (row shard x1, NCCL and the
+    # fused all-gather at world size 1) -- a check of this code path on a one-GPU box, not a bench line
+    sharded = world > 1 or os.environ.get("QP_BENCH_FORCE_SHARDED") == "1"
+    if sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     batch = args.batch
     layers = workload(world)
     cbs = {}
@@ -309,7 +314,7 @@ def main():
             cbs[key] = QL.Codebook(L["scheme"], L["bits_x4"], np.fromfile(tlut_file(*key)[0], dtype="<f2"), L=16)
     rots = {d_in: QL.Rht(SEED, d_in) for _, d_in in SHAPES}
     comm = None
-    if world > 1:
+    if sharded:
         uid = [QL.NcclComm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = QL.NcclComm(uid[0], world, rank)
@@ -323,8 +328,8 @@ def main():
             s = channel_scales(d_out, d_in)
             full = QL.Layer.from_codes(codes, s, d_out, d_in, L["scheme"], L["bits_x4"], cbs[(L["scheme"], L["bits_x4"])],
                                        rots[d_in])
-            lay = full.shard(rank, world) if world > 1 else full
-            if world > 1:
+            lay = full.shard(rank, world) if sharded else full
+            if sharded:
                 del full
             insts.append(dict(layer=lay, meta=L))
     # activations / outputs of a step live in one device buffer each (per replica), so the
@@ -363,7 +368,7 @@ def main():
             multis.append(QL.Multi([inst["layer"] for inst in insts[rep * n_layers:(rep + 1) * n_layers]]))
 
     # N > 1, fused all-gather: every replica's y_full buffers + flags, IPC-mapped across the ranks
-    pgs, allgather = [], args.allgather if (use_engine and world > 1) else None
+    pgs, allgather = [], args.allgather if (use_engine and sharded) else None
     if allgather == "p2p":
         for rep in range(REPLICAS):
             pgs.append(QL.MultiPeerGather(world, rank, [L["m"] for L in layers], batch, dtype=torch.float32))
@@ -381,7 +386,7 @@ def main():
 
     def fwd(inst, stream=None, flags=0):
         flags |= extra_flags
-        if world > 1:
+        if sharded:
             inst["layer"].forward_sharded(inst["x"], batch, inst["y"], comm, flags=flags, stream=stream)
         else:
             inst["layer"].forward(inst["x"], batch, inst["y"], flags=flags, stream=stream)
@@ -389,11 +394,11 @@ def main():
     def step_fn(rep, stream):
         """One step: the 9 layers of replica `rep` (rotation + fused dequant-GEMV each)."""
         group = insts[rep * n_layers:(rep + 1) * n_layers]
-        if use_engine and world > 1 and allgather == "p2p":
+        if use_engine and sharded and allgather == "p2p":
             # this rank's shards through the engine, whose epilogue stores every final value into
             # every rank's y_full (NVLink peer stores); one wait kernel for the deliveries
             pgs[rep].forward(multis[rep], [i["x"] for i in group], flags=extra_flags, stream=stream)
-        elif use_engine and world > 1:
+        elif use_engine and sharded:
             # this rank's shards through the engine, then one grouped NCCL all-gather of all 9 outputs
             multis[rep].forward_sharded([i["x"] for i in group], batch, [i["y"] for i in group], comm,
                                         flags=extra_flags, stream=stream)
@@ -437,7 +442,7 @@ def main():
     torch.cuda.synchronize()
 
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -455,7 +460,7 @@ def main():
         ev1.synchronize()
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
+    if sharded:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -573,7 +578,7 @@ def main():
     # the same steps with QP_INDEPENDENT (the caller's promise that no running work touches a step's
     # x / y: consecutive steps may overlap), reported beside the dependency-safe default
     indep = None
-    if use_engine and world == 1:
+    if use_engine and not sharded:
         gi = []
         with torch.cuda.stream(stream):
             for rep in range(REPLICAS):
@@ -606,7 +611,7 @@ def main():
         eng_us = time_engine(batch)
         rank_bytes = gemv_bytes / world + rht_bytes / world
         eng = {"achieved": rank_bytes / (eng_us * 1e-6) / 1e9, "us": eng_us, "bytes": rank_bytes}
-    if use_engine and world == 1:
+    if use_engine and not sharded:
         # the metric spans batch 1-8: the same step at the other batch sizes (engine launch alone)
         for b_ in (1, 2, 4, 8):
             if b_ == batch:
@@ -624,7 +629,7 @@ def main():
     # forward (one qp_multi_fwd), one D2H copy of the 9 results into pinned host memory -- captured with
     # the forwards in a CUDA graph per replica (as a serving loop would), timed with events.
     e2e = None
-    if world == 1:
+    if not sharded:
         hx = torch.empty(x_elems, dtype=torch.float16).pin_memory()
         hy = torch.empty(y_elems, dtype=torch.float32).pin_memory()
         hx.copy_(bufs[0][0].cpu())
@@ -720,7 +725,7 @@ def main():
                "serial_ms_per_step": round(e2e_ms_serial, 4)}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not sharded and not args.no_cpu_baseline:
         nb, dt = oracle_sample(layers, budget_rows=1536)
         cpu = {"value": round(nb / dt / 1e9, 6), "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
                "sample": "first 1536 rows of each of the 9 C2 layers: float64 decode + RHT + matvec (batch 1)",
@@ -742,7 +747,7 @@ def main():
                        "parallelism": ((f"row-shard x{world}: engine over each rank's shards with the all-gather "
                                         f"fused into its epilogue (peer stores over NVLink)" if allgather == "p2p" else
                                         f"row-shard x{world}: engine over each rank's shards + one grouped NCCL "
-                                        f"all-gather per step") if world > 1 else "single GPU"),
+                                        f"all-gather per step") if sharded else "single GPU"),
                        "l2": "inputs larger than L2 (2 replicas, 326 MB per 2 steps, L2 126 MB)",
                        "graph": "CUDA graph per step, PDL between consecutive kernels",
                        "kernels_per_layer": round(launches_per_step / n_layers, 3),
@@ -780,7 +785,7 @@ def main():
     if comm is not None:
         torch.cuda.synchronize()
         comm.close()
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 

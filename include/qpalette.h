@@ -201,9 +201,10 @@ qp_status qp_multi_fwd_sharded(qp_multi* m, const void* const* xs, qp_dtype xt, 
  * ys_peers[i * world + k]: rank k's y_full of layer i (dtype yt, mapped with qp_ipc_open; this rank's
  * own at k = rank), laid out identically on every rank: layer i's buffer at the same byte offset from
  * layer 0's on every rank (QP_ERR_INVALID_ARG otherwise); flag_peers[k]: rank k's flag array (unsigned[2 * world + 1], zeroed once), as in
- * qp_linear_fwd_sharded_p2p, whose round-entry barrier and y_full reuse rule apply (a rank stores
- * round n into a peer's y_full only after that peer entered round n); the call returns with a wait
- * kernel enqueued that completes once every rank's rows of every layer have arrived. Every layer
+ * qp_linear_fwd_sharded_p2p, whose y_full reuse rule applies (a rank stores round n into a peer's
+ * y_full only after that peer entered round n). Each engine launch of the call is one round, with the
+ * entry announcement, the entry gate, the delivery and the wait for every rank's delivery inside the
+ * kernel: the launch completes once every rank's rows of its layers have arrived. Every layer
  * must have an engine variant (QP_ERR_UNSUPPORTED otherwise); QP_Y_ACCUMULATE / QP_INDEPENDENT are
  * rejected (QP_ERR_INVALID_ARG). A peer that never arrives traps the wait kernel after 20 s. */
 qp_status qp_multi_fwd_sharded_p2p(qp_multi* m, const void* const* xs, qp_dtype xt, int batch,

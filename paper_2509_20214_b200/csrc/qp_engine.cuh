@@ -188,11 +188,51 @@ __device__ __forceinline__ void store_peers(const EngParams& p, const EngOp& o, 
 
 // The fused all-gather's launch-exit protocol: arrive = this CTA's peer stores fenced before its arrival
 // on the exit counter; deliver = the last CTA bumps this rank's delivery counter on every rank.
+// Flag array of a rank (unsigned[2 * world + 1], as qp_linear_fwd_sharded_p2p's): [k] deliveries from
+// rank k, [world] rounds this rank has consumed, [world + 1 + k] rounds rank k has entered. One engine
+// launch = one round: its CTA 0 announces the entry on every rank once the launch may run (after
+// griddepcontrol.wait: this rank's earlier stream work, incl. readers of the previous round's y_full,
+// is done); a warp's first peer store waits until every rank has entered the round; the last CTA out
+// delivers to every rank, waits for every rank's delivery and counts the round consumed -- so the
+// kernel's completion means every y_full holds every rank's rows (no enter / wait kernels: the PDL
+// chain between consecutive engine launches stays intact). A peer that never shows traps after 20 s.
+constexpr unsigned long long kEngPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long eng_gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// every rank's flag [base + k] >= want (k = 0 .. world-1)
+__device__ __forceinline__ void peer_wait_all(const unsigned* local, int base, int world, unsigned want) {
+  const unsigned long long t0 = eng_gtimer_ns();
+#pragma unroll 1
+  for (int k = 0; k < world; ++k)
+    while ((int)(ld_acquire_sys_u32(local + base + k) - want) < 0) {
+      if (eng_gtimer_ns() - t0 > kEngPeerTimeoutNs) __trap();
+      __nanosleep(64);
+    }
+}
+__device__ __forceinline__ void peer_enter(const EngParams& p) {
+  const int world = p.n_peers;
+#pragma unroll 1
+  for (int k = 0; k < world; ++k) atomicAdd_system(p.peer_flag[k] + world + 1 + p.peer_rank, 1u);
+}
 __device__ __forceinline__ void peer_fence() { __threadfence_system(); }
 __device__ __forceinline__ void peer_deliver(const EngParams& p) {
   __threadfence_system();
 #pragma unroll 1
   for (int k = 0; k < p.n_peers; ++k) atomicAdd_system(p.peer_flag[k] + p.peer_rank, 1u);
+  // every rank's rows of this round have arrived here, then the round is consumed
+  unsigned* local = p.peer_flag[p.peer_rank];
+  const unsigned round = local[p.n_peers] + 1u;
+  peer_wait_all(local, 0, p.n_peers, round);
+  local[p.n_peers] = round;
+  __threadfence_system();
 }
 
 // RP: row tiles per work unit. RP = 2 (batch >= 4): a unit is the two row tiles of a row pair at one
@@ -343,6 +383,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
 #pragma unroll 1
     for (int st = 0; st < NS; ++st) mbar_init(bars + 8u * st, 1);
     mbar_fence_init();
+    *reinterpret_cast<volatile unsigned*>(smem + PL::BAR_OFF + 512 + 4 * warp) = 0u;   // peer gate
   }
   __syncwarp();
   if (a < b) fetch_ahead(0, 0u, 0u, 0u, false, oi, rt, kt, left, opk);
@@ -352,6 +393,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
     for (int st = 1; st < NS && (uint32_t)st < ntiles; ++st)
       fetch_ahead(st, 0u, (uint32_t)st / RP, (uint32_t)st % RP, true, oi, rt, kt, left, opk);
   if (!rotor) order_before();
+  if (p.n_peers > 0 && blockIdx.x == 0 && tid == 0) peer_enter(p);   // this rank entered the round
   QP_TL(3);
   __syncthreads();
 
@@ -367,6 +409,16 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
   // needed, through an index the compiler cannot hoist (shfl of the layer index), so no per-layer
   // address set stays live across the decode.
   auto opaque = [&](int v) -> int { return __shfl_sync(0xffffffffu, v, 0); };
+  // fused all-gather: before this warp's first peer store of the launch, every rank has entered the
+  // round (a warp-private shared word remembers it; the upper half of the barrier area is unused)
+  volatile unsigned* gate = reinterpret_cast<volatile unsigned*>(smem + PL::BAR_OFF + 512) + warp;
+  auto peer_gate = [&]() {
+    if (*gate == 0u) {
+      const unsigned* local = p.peer_flag[p.peer_rank];
+      peer_wait_all(local, p.n_peers + 1, p.n_peers, local[p.n_peers] + 1u);
+      *gate = 1u;
+    }
+  };
   // wait until layer o_'s x' is complete in this launch (`ready` counts its finished rotation jobs
   // and is reset by the last CTA out): acquire polling
   auto enter_op = [&](int o_) {
@@ -511,6 +563,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
               if (bb < p.batch) {
                 const float v = acc[h][m][r] * sc[h][2 * m + (r >> 1)];
                 if (p.n_peers > 0) {
+                  peer_gate();
                   store_peers(p, p.op[oe], bb, rth * kTileRows + row, v);
                 } else {
                   const size_t e = (size_t)bb * d_out + rth * kTileRows + row;
@@ -549,6 +602,7 @@ __global__ void __launch_bounds__(EPlan<MODE, L, TB, REPS, CMIN, CMAX>::NWARP * 
               __stcg(wp, 0.f);
               const size_t ye = (size_t)bb * d_out + rth * kTileRows + row;
               if (p.n_peers > 0) {
+                peer_gate();
                 store_peers(p, p.op[oe], bb, rth * kTileRows + row, v);
               } else if (p.y_f32) {
                 float* y = reinterpret_cast<float*>(yv) + ye;

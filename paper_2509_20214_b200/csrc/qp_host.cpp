@@ -1425,10 +1425,10 @@ qp_status multi_fwd_impl(qp_multi* m, const void* const* xs, qp_dtype xt, int ba
 
 // Row-sharded multi-layer forward with the all-gather fused into the engine epilogue: every final y
 // value of this rank's rows is stored straight into every rank's y_full over NVLink (peer-mapped
-// pointers), the last CTA out of each engine launch delivers to every rank, and one wait kernel
-// consumes the deliveries -- no collective kernel, no gather scratch, no permutation (the stores
-// land in the [B][P m] layout). A round-entry barrier precedes the launch (the y_full reuse rule of
-// qp_linear_fwd_sharded_p2p).
+// pointers); the round protocol (entry announcement, per-warp entry gate before the first peer store,
+// delivery, wait for every rank's delivery) runs inside each engine launch -- no collective kernel,
+// no gather scratch, no permutation (the stores land in the [B][P m] layout), no extra kernels, so
+// consecutive launches keep their PDL overlap. The y_full reuse rule of qp_linear_fwd_sharded_p2p holds.
 extern "C" qp_status qp_multi_fwd_sharded_p2p(qp_multi* m, const void* const* xs, qp_dtype xt, int batch,
                                               void* const* ys_peers, unsigned* const* flag_peers, int rank,
                                               int world, qp_dtype yt, unsigned flags, void* stream) {
@@ -1462,18 +1462,14 @@ extern "C" qp_status qp_multi_fwd_sharded_p2p(qp_multi* m, const void* const* xs
                   "qp_linear_fwd_sharded_p2p per layer", gr.first);
     ++launches;
   }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (cudaError_t e = launch_peer_enter(flag_peers, rank, world, s); e != cudaSuccess)
-    return cuda_fail(e, "peer enter kernel launch");
+  // (each engine launch is one round: its entry announcement, the per-warp entry gate before the first
+  // peer store, the delivery and the wait for every rank's delivery all run inside the engine kernel)
+  (void)launches;
   const EngPeers pe{world, rank, ys_peers, flag_peers};
   // ys: this rank's own y_full (argument checks only; the engine stores through pe)
   std::vector<void*> own(n);
   for (int i = 0; i < n; ++i) own[i] = ys_peers[(size_t)i * world + rank];
-  qp_status st = multi_fwd_impl(m, xs, xt, batch, own.data(), yt, flags, stream, &pe);
-  if (st != QP_OK) return st;
-  if (cudaError_t e = launch_peer_wait(flag_peers[rank], world, s, launches); e != cudaSuccess)
-    return cuda_fail(e, "peer wait kernel launch");
-  return QP_OK;
+  return multi_fwd_impl(m, xs, xt, batch, own.data(), yt, flags, stream, &pe);
 }
 
 // Row-sharded multi-layer forward: the engine over this rank's shards (one persistent launch per
